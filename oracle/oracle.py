@@ -1,0 +1,102 @@
+"""ctypes wrapper of the C oracle (oracle/fs_oracle.c) -- TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline
+legs may import this module. It consumes the same lowered arrays as the CUDA
+engine (paper_2508_03148_b200.lower) and returns the same raw result layout,
+so parity checks compare like with like.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2508_03148_b200 import abi
+from paper_2508_03148_b200.engine import LogSpec, RawResults, alloc_results, make_log, soa
+from paper_2508_03148_b200.lower import Lowered
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "build", "libfsoracle.so")
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB):
+        build()
+    lib = ctypes.CDLL(LIB)
+    vp = ctypes.c_void_p
+    lib.fso_run_batch.restype = ctypes.c_int
+    lib.fso_run_batch.argtypes = [vp, ctypes.c_int32, vp, vp, vp, abi.RequestSoA, vp, vp,
+                                  abi.RequestOut, vp, ctypes.c_int]
+    lib.fso_router_seed.restype = ctypes.c_uint32
+    lib.fso_router_seed.argtypes = [vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int32]
+    lib.fso_routing_key.restype = None
+    lib.fso_routing_key.argtypes = [ctypes.c_uint64, vp]
+    lib.fso_route_uniform.restype = ctypes.c_int
+    lib.fso_route_uniform.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_uint64, vp]
+    lib.fso_attention_us.restype = ctypes.c_double
+    lib.fso_attention_us.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_int]
+    lib.fso_linear_us.restype = ctypes.c_double
+    lib.fso_linear_us.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_double] * 3 + [ctypes.c_int]
+    lib.fso_pysum.restype = ctypes.c_double
+    lib.fso_pysum.argtypes = [vp, ctypes.c_int]
+    abi.check_sizes(lib, "fso_struct_sizes")
+    _lib = lib
+    return lib
+
+
+def run(low: Lowered, log: LogSpec | None = None, threads: int = 1) -> RawResults:
+    lib = load()
+    res = alloc_results(low)
+    if log is not None:
+        res.log = make_log(low.n_instances, log)
+    pr = abi.RequestOut(abi.ptr(res.first_ns), abi.ptr(res.done_ns), abi.ptr(res.done_rank))
+    lib.fso_run_batch(abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas),
+                      abi.ptr(low.prefixes), abi.ptr(low.trace_counts), soa(low),
+                      abi.ptr(res.rows), abi.ptr(res.replica_out), pr,
+                      ctypes.byref(res.log.c_struct) if res.log is not None else None, threads)
+    return res
+
+
+def router_seed(prefix: str, mb: int, step: int, layer: int) -> int:
+    from paper_2508_03148_b200.lower import _prefix
+    rec = np.array(_prefix(prefix), dtype=abi.SEED_PREFIX)
+    return int(load().fso_router_seed(abi.ptr(rec), mb, step, layer))
+
+
+def routing_key(seed: int) -> tuple[int, int]:
+    k = np.zeros(2, dtype=np.uint64)
+    load().fso_routing_key(seed, abi.ptr(k))
+    return int(k[0]), int(k[1])
+
+
+def route_uniform(T: int, E: int, k: int, seed: int) -> tuple[list[int], int]:
+    c = np.zeros(E, dtype=np.int32)
+    st = load().fso_route_uniform(T, E, k, seed, abi.ptr(c))
+    return c.tolist(), st
+
+
+def attention_us(decode: bool, q, kv, hq, hkv, hd, peak, bw, ovh=5.0, dt=2) -> float:
+    q = np.ascontiguousarray(q, dtype=np.int64)
+    kv = np.ascontiguousarray(kv, dtype=np.int64)
+    return load().fso_attention_us(int(decode), abi.ptr(q), abi.ptr(kv), len(q), hq, hkv, hd,
+                                   peak, bw, ovh, dt)
+
+
+def pysum(xs) -> float:
+    a = np.ascontiguousarray(xs, dtype=np.float64)
+    return load().fso_pysum(abi.ptr(a), len(a))

@@ -1,0 +1,89 @@
+"""Batched entry points: `simulate(configs)` and `run_one(config)`.
+
+`simulate` is the data-parallel hot path: N config documents (or parsed
+DeploymentConfigs) are lowered once and stepped together on the GPU, one
+warp per instance; the result is one MetricsBundle -- or the exception the
+reference would have raised -- per instance, in input order. This replaces
+the reference's per-point loop over `run_one` (cli.py:82-102, 197-237).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+from .config import DeploymentConfig, parse_config
+from .engine import Engine, LogSpec, default_engine
+from .lower import InstanceSpec, Lowered, lower
+from .metrics import InstanceResult, MetricsBundle, compute_metrics, split_results
+
+
+@dataclass
+class Failure:
+    """A point that raised: mirrors the sweep's `failed: {Type}: {msg}` rows."""
+
+    exception: Exception
+
+    @property
+    def status(self) -> str:
+        return f"failed: {type(self.exception).__name__}: {self.exception}"
+
+
+def instance_spec(config: DeploymentConfig) -> InstanceSpec:
+    """What `run_one` builds before `make_simulation` (cli.py:84-94)."""
+    cm = config.cost_model
+    return InstanceSpec(
+        deployment=config.deployment(), requests=config.request_arrays(), policy=config.policy,
+        af=config.af if config.mode == "af" else None, routing=config.routing, seed=config.seed,
+        learned=bool(cm.attention_model_path or cm.grouped_gemm_model_path))
+
+
+@dataclass
+class BatchRun:
+    lowered: Lowered
+    results: list[InstanceResult]
+    seconds_lower: float
+    seconds_device: float
+
+
+def run_specs(specs: list[InstanceSpec], engine: Engine | None = None,
+              log: LogSpec | None = None) -> BatchRun:
+    eng = engine or default_engine()
+    t0 = time.perf_counter()
+    low = lower(specs)
+    t1 = time.perf_counter()
+    raw = eng.run(low, log=log)
+    t2 = time.perf_counter()
+    modes = [sp.deployment.mode for sp in specs]
+    return BatchRun(low, split_results(low, raw, modes), t1 - t0, t2 - t1)
+
+
+def simulate(configs: list, engine: Engine | None = None, base_dir: str = "."
+             ) -> list[MetricsBundle | Failure]:
+    """Simulate every config on the GPU; per-instance errors become Failure entries."""
+    out: list[MetricsBundle | Failure | None] = [None] * len(configs)
+    specs, where = [], []
+    for i, c in enumerate(configs):
+        try:
+            cfg = c if isinstance(c, DeploymentConfig) else parse_config(c, base_dir=base_dir)
+            specs.append(instance_spec(cfg))
+            where.append(i)
+        except Exception as exc:  # config-time failures (cli.py:229-233)
+            out[i] = Failure(exc)
+    if specs:
+        run = run_specs(specs, engine)
+        for i, res in zip(where, run.results):
+            out[i] = compute_metrics(res) if res.ok else Failure(res.error())
+    return out
+
+
+def run_one(config: DeploymentConfig, engine: Engine | None = None) -> dict:
+    """Single-instance drop-in for the reference's run_one (cli.py:82-102)."""
+    from .orchestrator import make_simulation
+    spec = instance_spec(config)
+    sim = make_simulation(config.mode, spec.deployment, spec.requests.to_requests(), spec.policy,
+                          af=spec.af, routing=spec.routing, seed=spec.seed, engine=engine)
+    sim.spec.learned = spec.learned
+    result = sim.run()
+    return {"config": config, "trace": result, "metrics": compute_metrics(result),
+            "config_hash": config.config_hash()}

@@ -1,0 +1,466 @@
+// fs_capi.cu -- the C ABI (include/frontier_b200.h): engine lifecycle, staging of
+// instance descriptors into HBM, kernel launches, result readback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "fs_engine.h"
+
+using fs::EngineParams;
+using fs::HEv;
+using fs::RepState;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct fs_engine {
+  int device = 0;
+  int n_sms = 148;
+  std::string err;
+  cudaStream_t stream = nullptr;
+  // inputs
+  DevBuf descs, reps, prefixes, mid, trace, arrival, prompt, output, id_rank, order;
+  // workspace
+  DevBuf first, done, rank, finish, home, lists, list_base, heap, heap_base, xfer, rstate, af_ffn,
+      af_base, work;
+  // outputs
+  DevBuf rows, rep_out;
+  // log mirrors
+  DevBuf lg_batch_base, lg_member_base, lg_moe_base, lg_route_base, lg_counts_base, lg_batches,
+      lg_members, lg_moe, lg_routes, lg_counts, lg_bcount, lg_rcount, lg_trunc;
+  // cost-model scratch
+  DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
+      c_layers, c_seeds, c_pf, c_mid;
+  int32_t n_inst = 0, n_reps = 0, n_prefixes = 0;
+  int64_t n_req = 0;
+  int staged = 0;
+  int last_launches = 0;
+  EngineParams params{};
+};
+
+#define FS_CHECK(call)                                                        \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      e->err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+      return (int)e_ ? (int)e_ : 1;                                           \
+    }                                                                         \
+  } while (0)
+
+template <typename T>
+static cudaError_t upload(DevBuf& b, const T* src, size_t n, cudaStream_t s) {
+  cudaError_t r = b.ensure(n * sizeof(T));
+  if (r != cudaSuccess) return r;
+  if (n && src) return cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s);
+  return cudaSuccess;
+}
+
+extern "C" {
+
+int fs_abi_version(void) { return FS_ABI_VERSION; }
+
+// sizes of the ABI structs, checked by the Python binding at load time
+int fs_struct_sizes(int64_t* out, int n) {
+  const int64_t s[] = {(int64_t)sizeof(fs_cost_ctx),     (int64_t)sizeof(fs_seed_prefix),
+                       (int64_t)sizeof(fs_replica_desc), (int64_t)sizeof(fs_instance_desc),
+                       (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
+                       (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
+                       (int64_t)sizeof(fs_attn_params)};
+  const int k = (int)(sizeof(s) / sizeof(s[0]));
+  for (int i = 0; i < n && i < k; i++) out[i] = s[i];
+  return k;
+}
+
+int fs_create(int device, fs_engine** out) {
+  if (!out) return 1;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return 2;
+  if (device < 0 || device >= count) return 3;
+  if (cudaSetDevice(device) != cudaSuccess) return 4;
+  fs_engine* e = new fs_engine();
+  e->device = device;
+  cudaDeviceGetAttribute(&e->n_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete e;
+    return 5;
+  }
+  *out = e;
+  return 0;
+}
+
+void fs_destroy(fs_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+const char* fs_last_error(const fs_engine* e) { return e ? e->err.c_str() : "null engine"; }
+
+int fs_last_launch_count(const fs_engine* e) { return e ? e->last_launches : 0; }
+
+int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
+             const fs_replica_desc* replicas, int32_t n_replicas, const fs_seed_prefix* prefixes,
+             int32_t n_prefixes, const int64_t* trace_counts, int64_t n_trace_counts,
+             fs_request_soa rq, int64_t n_requests) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  e->err.clear();
+  cudaStream_t s = e->stream;
+  // host-side workspace layout
+  std::vector<int64_t> list_base(n_instances), heap_base(n_instances), af_base(n_instances);
+  int64_t lb = 0, hb = 0, ab = 0;
+  for (int i = 0; i < n_instances; i++) {
+    const fs_instance_desc& d = descs[i];
+    if (d.n_requests < 0 || d.n_replicas < 1 || d.req_offset < 0 ||
+        d.req_offset + d.n_requests > n_requests || d.replica_offset < 0 ||
+        d.replica_offset + d.n_replicas > n_replicas) {
+      e->err = "instance " + std::to_string(i) + ": offsets out of range";
+      return 10;
+    }
+    for (int r = 0; r < d.n_replicas; r++) {
+      const fs_replica_desc& rd = replicas[d.replica_offset + r];
+      if (rd.prefix < 0 || rd.prefix >= n_prefixes || rd.prefix_mb >= n_prefixes) {
+        e->err = "instance " + std::to_string(i) + ": prefix index out of range";
+        return 11;
+      }
+    }
+    list_base[i] = lb;
+    lb += 3LL * d.n_replicas * std::max(d.n_requests, 1);
+    heap_base[i] = hb;
+    hb += (int64_t)d.n_replicas + d.n_requests + 8;
+    if (d.mode == FS_MODE_AF) {
+      af_base[i] = ab;
+      ab += (int64_t)std::min(std::max(d.af_micro_batches, 1), FS_MAX_MICRO_BATCHES) *
+            std::max(d.num_layers, 1);
+    } else {
+      af_base[i] = -1;
+    }
+  }
+  // longest estimated cost first (the work queue is consumed in this order)
+  std::vector<int32_t> order(n_instances);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return descs[a].est_cost > descs[b].est_cost; });
+
+  FS_CHECK(upload(e->descs, descs, n_instances, s));
+  FS_CHECK(upload(e->reps, replicas, n_replicas, s));
+  FS_CHECK(upload(e->prefixes, prefixes, n_prefixes, s));
+  FS_CHECK(e->mid.ensure((size_t)std::max(n_prefixes, 1) * 8 * sizeof(uint32_t)));
+  FS_CHECK(upload(e->trace, trace_counts, (size_t)n_trace_counts, s));
+  FS_CHECK(upload(e->arrival, rq.arrival_ns, (size_t)n_requests, s));
+  FS_CHECK(upload(e->prompt, rq.prompt_tokens, (size_t)n_requests, s));
+  FS_CHECK(upload(e->output, rq.output_tokens, (size_t)n_requests, s));
+  FS_CHECK(upload(e->id_rank, rq.id_rank, (size_t)n_requests, s));
+  FS_CHECK(upload(e->order, order.data(), order.size(), s));
+  FS_CHECK(upload(e->list_base, list_base.data(), list_base.size(), s));
+  FS_CHECK(upload(e->heap_base, heap_base.data(), heap_base.size(), s));
+  FS_CHECK(upload(e->af_base, af_base.data(), af_base.size(), s));
+  const size_t nr = (size_t)std::max<int64_t>(n_requests, 1);
+  FS_CHECK(e->first.ensure(nr * 8));
+  FS_CHECK(e->done.ensure(nr * 8));
+  FS_CHECK(e->rank.ensure(nr * 4));
+  FS_CHECK(e->finish.ensure(nr * 4));
+  FS_CHECK(e->home.ensure(nr * 4));
+  FS_CHECK(e->xfer.ensure(nr * 4));
+  FS_CHECK(e->lists.ensure((size_t)std::max<int64_t>(lb, 1) * 4));
+  FS_CHECK(e->heap.ensure((size_t)std::max<int64_t>(hb, 1) * sizeof(HEv)));
+  FS_CHECK(e->rstate.ensure((size_t)std::max(n_replicas, 1) * sizeof(RepState)));
+  FS_CHECK(e->af_ffn.ensure((size_t)std::max<int64_t>(ab, 1) * 8));
+  FS_CHECK(e->work.ensure(sizeof(int32_t)));
+  FS_CHECK(e->rows.ensure((size_t)std::max(n_instances, 1) * sizeof(fs_metric_row)));
+  FS_CHECK(e->rep_out.ensure((size_t)std::max(n_replicas, 1) * sizeof(fs_replica_out)));
+  // done_ns / first_ns start at -1 so a request the engine never reached is visible
+  FS_CHECK(cudaMemsetAsync(e->first.p, 0xff, nr * 8, s));
+  FS_CHECK(cudaMemsetAsync(e->done.p, 0xff, nr * 8, s));
+  FS_CHECK(cudaMemsetAsync(e->rank.p, 0xff, nr * 4, s));
+
+  EngineParams& P = e->params;
+  memset(&P, 0, sizeof P);
+  P.descs = e->descs.as<fs_instance_desc>();
+  P.n_inst = n_instances;
+  P.reps = e->reps.as<fs_replica_desc>();
+  P.prefixes = e->prefixes.as<fs_seed_prefix>();
+  P.midstate = e->mid.as<uint32_t>();
+  P.trace_counts = e->trace.as<int64_t>();
+  P.arrival = e->arrival.as<int64_t>();
+  P.prompt = e->prompt.as<int32_t>();
+  P.output = e->output.as<int32_t>();
+  P.id_rank = e->id_rank.as<int32_t>();
+  P.order = e->order.as<int32_t>();
+  P.first_ns = e->first.as<int64_t>();
+  P.done_ns = e->done.as<int64_t>();
+  P.done_rank = e->rank.as<int32_t>();
+  P.finish_at = e->finish.as<int32_t>();
+  P.home = e->home.as<int32_t>();
+  P.lists = e->lists.as<int32_t>();
+  P.list_base = e->list_base.as<int64_t>();
+  P.heap = e->heap.as<HEv>();
+  P.heap_base = e->heap_base.as<int64_t>();
+  P.xfer = e->xfer.as<int32_t>();
+  P.rstate = e->rstate.as<RepState>();
+  P.af_ffn = e->af_ffn.as<int64_t>();
+  P.af_base = e->af_base.as<int64_t>();
+  P.rows = e->rows.as<fs_metric_row>();
+  P.rep_out = e->rep_out.as<fs_replica_out>();
+  P.work_counter = e->work.as<int32_t>();
+  P.log_enabled = 0;
+  e->n_inst = n_instances;
+  e->n_reps = n_replicas;
+  e->n_prefixes = n_prefixes;
+  e->n_req = n_requests;
+  fs::launch_midstate(P.prefixes, e->mid.as<uint32_t>(), n_prefixes, s);
+  FS_CHECK(cudaGetLastError());
+  FS_CHECK(cudaStreamSynchronize(s));
+  e->staged = 1;
+  return 0;
+}
+
+int fs_launch_async(fs_engine* e, void* stream) {
+  if (!e || !e->staged) return 1;
+  cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+  FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
+  e->last_launches = 0;
+  e->last_launches += fs::launch_simulation(e->params, e->n_sms, s);
+  e->last_launches += fs::launch_metrics(e->params, s);
+  FS_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int fs_fetch(fs_engine* e, fs_metric_row* rows_out, fs_replica_out* replica_out,
+             fs_request_out pr) {
+  if (!e || !e->staged) return 1;
+  cudaStream_t s = e->stream;
+  FS_CHECK(cudaDeviceSynchronize());
+  if (rows_out)
+    FS_CHECK(cudaMemcpyAsync(rows_out, e->rows.p, sizeof(fs_metric_row) * e->n_inst,
+                             cudaMemcpyDeviceToHost, s));
+  if (replica_out)
+    FS_CHECK(cudaMemcpyAsync(replica_out, e->rep_out.p, sizeof(fs_replica_out) * e->n_reps,
+                             cudaMemcpyDeviceToHost, s));
+  if (pr.first_token_ns)
+    FS_CHECK(cudaMemcpyAsync(pr.first_token_ns, e->first.p, 8 * e->n_req, cudaMemcpyDeviceToHost, s));
+  if (pr.done_ns)
+    FS_CHECK(cudaMemcpyAsync(pr.done_ns, e->done.p, 8 * e->n_req, cudaMemcpyDeviceToHost, s));
+  if (pr.completion_rank)
+    FS_CHECK(cudaMemcpyAsync(pr.completion_rank, e->rank.p, 4 * e->n_req, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+static int64_t log_total(const int64_t* base, int n, int32_t cap) {
+  int64_t t = 0;
+  for (int i = 0; i < n; i++) t = std::max(t, base[i] + cap);
+  return t;
+}
+
+int fs_run_batch(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
+                 const fs_replica_desc* replicas, int32_t n_replicas,
+                 const fs_seed_prefix* prefixes, int32_t n_prefixes, const int64_t* trace_counts,
+                 int64_t n_trace_counts, fs_request_soa requests, int64_t n_requests,
+                 fs_metric_row* rows_out, fs_replica_out* replica_out, fs_request_out pr,
+                 fs_log* log) {
+  int rc = fs_stage(e, descs, n_instances, replicas, n_replicas, prefixes, n_prefixes,
+                    trace_counts, n_trace_counts, requests, n_requests);
+  if (rc) return rc;
+  cudaStream_t s = e->stream;
+  int64_t nb = 0, nm = 0, ne = 0, nro = 0, nc = 0;
+  if (log) {
+    // device mirror of the caller's log buffers
+    nb = log->batches ? log_total(log->batch_base, n_instances, log->batch_cap) : 0;
+    nm = log->members ? log_total(log->member_base, n_instances, log->member_cap) : 0;
+    ne = log->moe_ratio ? log_total(log->moe_base, n_instances, log->moe_cap) : 0;
+    nro = log->routes ? log_total(log->route_base, n_instances, log->route_cap) : 0;
+    nc = log->counts ? log_total(log->counts_base, n_instances, log->counts_cap) : 0;
+    fs_log& dl = e->params.log;
+    memset(&dl, 0, sizeof dl);
+    dl.batch_cap = log->batch_cap; dl.member_cap = log->member_cap; dl.moe_cap = log->moe_cap;
+    dl.route_cap = log->route_cap; dl.counts_cap = log->counts_cap;
+    const int64_t zero = 0;
+    (void)zero;
+    std::vector<int64_t> zeros(n_instances, 0);
+    FS_CHECK(upload(e->lg_batch_base, log->batch_base ? log->batch_base : zeros.data(), n_instances, s));
+    FS_CHECK(upload(e->lg_member_base, log->member_base ? log->member_base : zeros.data(), n_instances, s));
+    FS_CHECK(upload(e->lg_moe_base, log->moe_base ? log->moe_base : zeros.data(), n_instances, s));
+    FS_CHECK(upload(e->lg_route_base, log->route_base ? log->route_base : zeros.data(), n_instances, s));
+    FS_CHECK(upload(e->lg_counts_base, log->counts_base ? log->counts_base : zeros.data(), n_instances, s));
+    dl.batch_base = e->lg_batch_base.as<int64_t>();
+    dl.member_base = e->lg_member_base.as<int64_t>();
+    dl.moe_base = e->lg_moe_base.as<int64_t>();
+    dl.route_base = e->lg_route_base.as<int64_t>();
+    dl.counts_base = e->lg_counts_base.as<int64_t>();
+    if (nb) { FS_CHECK(e->lg_batches.ensure(nb * sizeof(fs_batch_rec))); dl.batches = e->lg_batches.as<fs_batch_rec>(); }
+    if (nm) { FS_CHECK(e->lg_members.ensure(nm * 4)); dl.members = e->lg_members.as<int32_t>(); }
+    if (ne) { FS_CHECK(e->lg_moe.ensure(ne * 8)); dl.moe_ratio = e->lg_moe.as<double>(); }
+    if (nro) { FS_CHECK(e->lg_routes.ensure(nro * sizeof(fs_route_rec))); dl.routes = e->lg_routes.as<fs_route_rec>(); }
+    if (nc) { FS_CHECK(e->lg_counts.ensure(nc * 4)); dl.counts = e->lg_counts.as<int32_t>(); }
+    FS_CHECK(e->lg_bcount.ensure(4 * (size_t)std::max(n_instances, 1)));
+    FS_CHECK(e->lg_rcount.ensure(4 * (size_t)std::max(n_instances, 1)));
+    FS_CHECK(e->lg_trunc.ensure(4 * (size_t)std::max(n_instances, 1)));
+    FS_CHECK(cudaMemsetAsync(e->lg_bcount.p, 0, 4 * (size_t)n_instances, s));
+    FS_CHECK(cudaMemsetAsync(e->lg_rcount.p, 0, 4 * (size_t)n_instances, s));
+    FS_CHECK(cudaMemsetAsync(e->lg_trunc.p, 0, 4 * (size_t)n_instances, s));
+    dl.batch_count = e->lg_bcount.as<int32_t>();
+    dl.route_count = e->lg_rcount.as<int32_t>();
+    dl.truncated = e->lg_trunc.as<int32_t>();
+    e->params.log_enabled = 1;
+  }
+  rc = fs_launch_async(e, s);
+  if (rc) { e->params.log_enabled = 0; return rc; }
+  rc = fs_fetch(e, rows_out, replica_out, pr);
+  if (!rc && log) {
+    if (nb) FS_CHECK(cudaMemcpy(log->batches, e->lg_batches.p, nb * sizeof(fs_batch_rec), cudaMemcpyDeviceToHost));
+    if (nm) FS_CHECK(cudaMemcpy(log->members, e->lg_members.p, nm * 4, cudaMemcpyDeviceToHost));
+    if (ne) FS_CHECK(cudaMemcpy(log->moe_ratio, e->lg_moe.p, ne * 8, cudaMemcpyDeviceToHost));
+    if (nro) FS_CHECK(cudaMemcpy(log->routes, e->lg_routes.p, nro * sizeof(fs_route_rec), cudaMemcpyDeviceToHost));
+    if (nc) FS_CHECK(cudaMemcpy(log->counts, e->lg_counts.p, nc * 4, cudaMemcpyDeviceToHost));
+    if (log->batch_count) FS_CHECK(cudaMemcpy(log->batch_count, e->lg_bcount.p, 4 * (size_t)n_instances, cudaMemcpyDeviceToHost));
+    if (log->route_count) FS_CHECK(cudaMemcpy(log->route_count, e->lg_rcount.p, 4 * (size_t)n_instances, cudaMemcpyDeviceToHost));
+    if (log->truncated) FS_CHECK(cudaMemcpy(log->truncated, e->lg_trunc.p, 4 * (size_t)n_instances, cudaMemcpyDeviceToHost));
+  }
+  e->params.log_enabled = 0;
+  memset(&e->params.log, 0, sizeof e->params.log);
+  return rc;
+}
+
+int fs_attention_cost_dev(fs_engine* e, const int32_t* q_lens, const int32_t* kv_lens,
+                          const int64_t* offsets, const uint8_t* is_decode, int64_t n_batches,
+                          fs_attn_params params, double* out_us, int32_t* status, void* stream) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+  e->last_launches = fs::launch_attention_cost(q_lens, kv_lens, offsets, is_decode, n_batches,
+                                               params, out_us, status, e->n_sms, s);
+  FS_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int fs_attention_cost(fs_engine* e, const int32_t* q_lens, const int32_t* kv_lens,
+                      const int64_t* offsets, const uint8_t* is_decode, int64_t n_batches,
+                      fs_attn_params params, double* out_us, int32_t* status) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  const int64_t n_el = n_batches > 0 ? offsets[n_batches] : 0;
+  FS_CHECK(upload(e->c_q, q_lens, (size_t)n_el, s));
+  FS_CHECK(upload(e->c_kv, kv_lens, (size_t)n_el, s));
+  FS_CHECK(upload(e->c_off, offsets, (size_t)n_batches + 1, s));
+  FS_CHECK(upload(e->c_dec, is_decode, (size_t)n_batches, s));
+  FS_CHECK(e->c_out.ensure((size_t)std::max<int64_t>(n_batches, 1) * 8));
+  FS_CHECK(e->c_status.ensure((size_t)std::max<int64_t>(n_batches, 1) * 4));
+  int rc = fs_attention_cost_dev(e, e->c_q.as<int32_t>(), e->c_kv.as<int32_t>(),
+                                 e->c_off.as<int64_t>(), e->c_dec.as<uint8_t>(), n_batches, params,
+                                 e->c_out.as<double>(), e->c_status.as<int32_t>(), s);
+  if (rc) return rc;
+  FS_CHECK(cudaMemcpyAsync(out_us, e->c_out.p, 8 * n_batches, cudaMemcpyDeviceToHost, s));
+  if (status) FS_CHECK(cudaMemcpyAsync(status, e->c_status.p, 4 * n_batches, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fs_attention_features_dev(fs_engine* e, const int32_t* q_lens, const int32_t* kv_lens,
+                              const int64_t* offsets, const uint8_t* is_decode, int64_t n_batches,
+                              fs_attn_params params, double* out17, void* stream) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+  e->last_launches = fs::launch_attention_features(q_lens, kv_lens, offsets, is_decode, n_batches,
+                                                   params, out17, s);
+  FS_CHECK(cudaGetLastError());
+  return 0;
+}
+
+// host-buffer variant of the features kernel (used by parity tests)
+int fs_attention_features(fs_engine* e, const int32_t* q_lens, const int32_t* kv_lens,
+                          const int64_t* offsets, const uint8_t* is_decode, int64_t n_batches,
+                          fs_attn_params params, double* out17) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  const int64_t n_el = n_batches > 0 ? offsets[n_batches] : 0;
+  FS_CHECK(upload(e->c_q, q_lens, (size_t)n_el, s));
+  FS_CHECK(upload(e->c_kv, kv_lens, (size_t)n_el, s));
+  FS_CHECK(upload(e->c_off, offsets, (size_t)n_batches + 1, s));
+  FS_CHECK(upload(e->c_dec, is_decode, (size_t)n_batches, s));
+  FS_CHECK(e->c_out.ensure((size_t)std::max<int64_t>(n_batches, 1) * 17 * 8));
+  int rc = fs_attention_features_dev(e, e->c_q.as<int32_t>(), e->c_kv.as<int32_t>(),
+                                     e->c_off.as<int64_t>(), e->c_dec.as<uint8_t>(), n_batches,
+                                     params, e->c_out.as<double>(), s);
+  if (rc) return rc;
+  FS_CHECK(cudaMemcpyAsync(out17, e->c_out.p, 17 * 8 * n_batches, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
+                     int32_t num_experts, int32_t top_k, int32_t* counts_out, int32_t* status) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  FS_CHECK(upload(e->c_tok, tokens, (size_t)n_calls, s));
+  FS_CHECK(upload(e->c_seed, seeds, (size_t)n_calls, s));
+  const size_t nc = (size_t)std::max(n_calls, 1) * std::max(num_experts, 1);
+  FS_CHECK(e->c_counts.ensure(nc * 4));
+  FS_CHECK(e->c_status.ensure((size_t)std::max(n_calls, 1) * 4));
+  e->last_launches = fs::launch_route_uniform(e->c_tok.as<int64_t>(), e->c_seed.as<uint64_t>(),
+                                              n_calls, num_experts, top_k,
+                                              e->c_counts.as<int32_t>(), e->c_status.as<int32_t>(), s);
+  FS_CHECK(cudaGetLastError());
+  FS_CHECK(cudaMemcpyAsync(counts_out, e->c_counts.p, 4 * (size_t)n_calls * num_experts,
+                           cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaMemcpyAsync(status, e->c_status.p, 4 * (size_t)n_calls, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fs_router_seeds(fs_engine* e, const fs_seed_prefix* prefixes, const int32_t* prefix_idx,
+                    const int32_t* micro_batch, const int64_t* steps, const int32_t* layers,
+                    int32_t n, uint32_t* seeds_out) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  int np = 0;
+  for (int i = 0; i < n; i++) np = std::max(np, prefix_idx[i] + 1);
+  FS_CHECK(upload(e->c_pf, prefixes, (size_t)np, s));
+  FS_CHECK(e->c_mid.ensure((size_t)std::max(np, 1) * 32));
+  fs::launch_midstate(e->c_pf.as<fs_seed_prefix>(), e->c_mid.as<uint32_t>(), np, s);
+  FS_CHECK(upload(e->c_pidx, prefix_idx, (size_t)n, s));
+  FS_CHECK(upload(e->c_mb, micro_batch, (size_t)n, s));
+  FS_CHECK(upload(e->c_steps, steps, (size_t)n, s));
+  FS_CHECK(upload(e->c_layers, layers, (size_t)n, s));
+  FS_CHECK(e->c_seeds.ensure((size_t)std::max(n, 1) * 4));
+  e->last_launches = 1 + fs::launch_router_seeds(e->c_pf.as<fs_seed_prefix>(), e->c_mid.as<uint32_t>(),
+                                                 e->c_pidx.as<int32_t>(), e->c_mb.as<int32_t>(),
+                                                 e->c_steps.as<int64_t>(), e->c_layers.as<int32_t>(),
+                                                 n, e->c_seeds.as<uint32_t>(), s);
+  FS_CHECK(cudaGetLastError());
+  FS_CHECK(cudaMemcpyAsync(seeds_out, e->c_seeds.p, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+}  // extern "C"

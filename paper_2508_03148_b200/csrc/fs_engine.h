@@ -1,0 +1,87 @@
+// fs_engine.h -- internal types shared by the kernels and the C-ABI host code.
+#pragma once
+#include <cstdint>
+
+#include "../../include/frontier_b200.h"
+
+namespace fs {
+
+// One stored event (state-changing kinds only).
+struct HEv {
+  int64_t t;
+  int64_t seq;
+  int32_t kind;
+  int32_t a;   // replica (local index)
+  int64_t b;   // duration (BATCH_COMPLETE) or request (KV done)
+};
+
+// Mutable per-replica state (global replica index).
+struct RepState {
+  int64_t used;          // KV pool used tokens
+  int64_t outstanding;   // sum of prompt tokens in the queue (pd.py:40-45)
+  int64_t steps;         // steps_executed
+  int64_t busy_ns;       // sum of BATCH_COMPLETE durations
+  int64_t sum_ctx;       // sum of (prompt + emitted) over the running list
+  int64_t inflight_dur;
+  int32_t qlen, rlen, ilen;
+  int32_t busy, start_pending;
+  int32_t dstep;         // decode iterations completed
+  int32_t min_finish;    // earliest finish step among running requests
+  int32_t inflight_phase;
+  int32_t inflight_moe;  // a moe-ratio log slot was written for the in-flight batch
+  int32_t pad;
+};
+
+struct EngineParams {
+  // inputs
+  const fs_instance_desc* descs;
+  int32_t n_inst;
+  const fs_replica_desc* reps;
+  const fs_seed_prefix* prefixes;
+  const uint32_t* midstate;      // 8 words per prefix (device-computed)
+  const int64_t* trace_counts;
+  const int64_t* arrival;
+  const int32_t* prompt;
+  const int32_t* output;
+  const int32_t* id_rank;
+  const int32_t* order;          // processing order (longest estimated first)
+  // workspace
+  int64_t* first_ns;
+  int64_t* done_ns;
+  int32_t* done_rank;
+  int32_t* finish_at;
+  int32_t* home;                 // prefill home (PD)
+  int32_t* lists;
+  const int64_t* list_base;      // per instance
+  HEv* heap;
+  const int64_t* heap_base;      // per instance
+  int32_t* xfer;                 // transfer FIFO ring, indexed like requests
+  RepState* rstate;
+  int64_t* af_ffn;
+  const int64_t* af_base;        // per instance (-1 when not AF)
+  // outputs
+  fs_metric_row* rows;
+  fs_replica_out* rep_out;
+  // optional log (device pointers)
+  fs_log log;
+  int32_t log_enabled;
+  int32_t* work_counter;
+};
+
+// host-side launchers (fs_engine.cu / fs_metrics.cu / fs_costs.cu)
+void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void* stream);
+int launch_simulation(const EngineParams& p, int n_sms, void* stream);
+int launch_metrics(const EngineParams& p, void* stream);
+int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,
+                          const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out,
+                          int32_t* status, int n_sms, void* stream);
+int launch_attention_features(const int32_t* q, const int32_t* kv, const int64_t* off,
+                              const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out17,
+                              void* stream);
+int launch_route_uniform(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
+                         int32_t* counts, int32_t* status, void* stream);
+int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int32_t* pidx,
+                        const int32_t* mb, const int64_t* steps, const int32_t* layers, int n,
+                        uint32_t* out, void* stream);
+
+}  // namespace fs

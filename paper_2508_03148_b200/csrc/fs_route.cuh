@@ -1,0 +1,169 @@
+// fs_route.cuh -- warp-cooperative uniform MoE routing + MoE layer cost.
+//
+// route_tokens(T, E, k, "uniform", seed)  costmodel/routing.py:65-113
+// moe_layer_latency                        costmodel/moe.py:69-128
+//
+// Layout: row r of the T x E key matrix is split into `nseg` contiguous
+// segments; lane (r mod rows_per_pass) * nseg + s generates segment s of row r
+// from its own Philox blocks, keeps the (k+1) smallest 53-bit keys packed with
+// the expert index ((u >> 11) << 11 | e) in registers, and the nseg lanes of a
+// row merge their lists with butterfly shuffles. The k smallest are tallied
+// into a per-warp shared-memory histogram; the (k+1)-th is kept only to detect
+// an exact tie at the selection boundary (argpartition would pick arbitrarily).
+#pragma once
+#include "fs_device.cuh"
+
+namespace fs {
+
+template <int KCAP>
+__device__ __forceinline__ void topk_insert(uint64_t (&top)[KCAP], int kc, uint64_t x,
+                                            uint64_t& thr) {
+  if (x >= thr) return;
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) {
+    if (j < kc) {
+      uint64_t lo = top[j] < x ? top[j] : x;
+      x = top[j] < x ? x : top[j];
+      top[j] = lo;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KCAP; j++)
+    if (j == kc - 1) thr = top[j];
+}
+
+// Returns FS_OK or FS_ERR_ROUTING_TIE. counts[] (shared, >= E ints) receives the tally.
+template <int KCAP>
+__device__ int route_uniform_warp_k(int lane, int64_t T, int E, int k, uint64_t k0, uint64_t k1,
+                                    int* counts) {
+  for (int e = lane; e < E; e += 32) counts[e] = 0;
+  __syncwarp();
+  if (T == 0) return FS_OK;
+  if (k == E) {
+    for (int e = lane; e < E; e += 32) counts[e] = (int)T;
+    __syncwarp();
+    return FS_OK;
+  }
+  const int kc = k + 1;  // keep one extra to detect boundary ties
+  int nseg = 1;
+  if (T < 16) {
+    int cap = (int)(32 / T);
+    while (nseg * 2 <= cap && nseg * 2 <= E) nseg *= 2;
+  }
+  const int rows_per_pass = 32 / nseg;
+  const int seg_len = (E + nseg - 1) / nseg;
+  const int my_row_in_pass = lane / nseg, my_seg = lane % nseg;
+  int tie = 0;
+  for (int64_t r0 = 0; r0 < T; r0 += rows_per_pass) {
+    const int64_t row = r0 + my_row_in_pass;
+    const bool active = my_row_in_pass < rows_per_pass && row < T;
+    uint64_t top[KCAP];
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) top[j] = ~0ull;
+    uint64_t thr = ~0ull;
+    if (active) {
+      const int e0 = my_seg * seg_len;
+      const int e1 = min(E, e0 + seg_len);
+      uint64_t n = (uint64_t)row * (uint64_t)E + (uint64_t)e0;
+      U4 blk;
+      if (e0 < e1) blk = philox4x64_10(n / 4 + 1, k0, k1);
+      for (int e = e0; e < e1; e++, n++) {
+        const int w = (int)(n & 3);
+        if (w == 0 && e != e0) blk = philox4x64_10(n / 4 + 1, k0, k1);
+        const uint64_t packed = ((blk.v[w] >> 11) << 11) | (uint64_t)e;
+        topk_insert<KCAP>(top, kc, packed, thr);
+      }
+    }
+    // merge the nseg partial lists of each row (all lanes participate in shuffles)
+    for (int s = 1; s < nseg; s <<= 1) {
+      uint64_t other[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, top[j], s);
+#pragma unroll
+      for (int j = 0; j < KCAP; j++)
+        if (j < kc) topk_insert<KCAP>(top, kc, other[j], thr);
+    }
+    if (active && my_seg == 0) {
+      uint64_t kth = 0, next = 0;
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) {
+        if (j < k) atomicAdd(&counts[(int)(top[j] & 0x7FF)], 1);
+        if (j == k - 1) kth = top[j];
+        if (j == k) next = top[j];
+      }
+      if ((kth >> 11) == (next >> 11)) tie = 1;
+    }
+  }
+  __syncwarp();
+  tie = __any_sync(FS_FULL, tie);
+  return tie ? FS_ERR_ROUTING_TIE : FS_OK;
+}
+
+__device__ inline int route_uniform_warp(int lane, int64_t T, int E, int k, uint64_t k0,
+                                         uint64_t k1, int* counts) {
+  if (k + 1 <= 4) return route_uniform_warp_k<4>(lane, T, E, k, k0, k1, counts);
+  if (k + 1 <= 9) return route_uniform_warp_k<9>(lane, T, E, k, k0, k1, counts);
+  return route_uniform_warp_k<FS_MAX_TOPK + 1>(lane, T, E, k, k0, k1, counts);
+}
+
+// moe_layer_latency from a tally in shared memory. All lanes return the same
+// total; *ratio (if non-null) gets expert / mean(per_rank) (base.py:247-252).
+// Returns FS_OK or a status.
+__device__ inline int moe_layer_warp(int lane, const int* counts, int64_t T, int E, int top_k,
+                                     int d_model, int expert_d_ff, int nm, int dt, int ep,
+                                     int moe_tp, double lat, double bw, const fs_cost_ctx& c,
+                                     double* total, double* ratio) {
+  if (ep < 1 || moe_tp < 1 || E % ep != 0 || expert_d_ff % moe_tp != 0)
+    return FS_ERR_TOPOLOGY_MISMATCH;
+  if (T < 1) return FS_ERR_EMPTY_BATCH;
+  double gate = linear_us(T, E, d_model, c, dt);
+  int64_t routed_bytes = T * (int64_t)top_k * d_model * dt;
+  double bpr = i2d(routed_bytes) / (double)ep;
+  double dispatch = collective_flt(false, bpr, ep, lat, bw) * 1e6;
+  const int per = E / ep;
+  const int64_t dffs = expert_d_ff / moe_tp;
+  // lane-local max over its ranks (ranks visited in increasing order)
+  double best = -1.0;
+  int best_r = 0x7fffffff;
+  for (int r = lane; r < ep; r += 32) {
+    int64_t routed = 0, active = 0;
+    for (int j = 0; j < per; j++) {
+      int cnt = counts[r * per + j];
+      routed += cnt;
+      active += cnt > 0;
+    }
+    double v = routed ? grouped_gemm_us(routed, active, d_model, dffs, nm, c, dt) : 0.0;
+    if (v > best) { best = v; best_r = r; }
+  }
+  // warp arg-max, first index wins ties (per_rank.index(max), moe.py:115-116)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    double ob = __shfl_xor_sync(FS_FULL, best, o);
+    int orr = __shfl_xor_sync(FS_FULL, best_r, o);
+    if (ob > best || (ob == best && orr < best_r)) { best = ob; best_r = orr; }
+  }
+  double expert = best;
+  double t = gate + dispatch;
+  t = t + expert;
+  t = t + dispatch;
+  *total = t;
+  if (ratio) {
+    // sum(per_rank_us) in rank order (Neumaier) -- recomputed serially by every lane
+    PySum ps;
+    ps.init();
+    for (int r = 0; r < ep; r++) {
+      int64_t routed = 0, active = 0;
+      for (int j = 0; j < per; j++) {
+        int cnt = counts[r * per + j];
+        routed += cnt;
+        active += cnt > 0;
+      }
+      ps.add(routed ? grouped_gemm_us(routed, active, d_model, dffs, nm, c, dt) : 0.0);
+    }
+    double s = ps.result();
+    *ratio = s > 0 ? expert / (s / (double)ep) : 1.0;
+  }
+  return FS_OK;
+}
+
+}  // namespace fs

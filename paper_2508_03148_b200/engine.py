@@ -1,0 +1,330 @@
+"""ctypes binding of libfrontier_b200.so (include/frontier_b200.h).
+
+The engine library is the only compute path: if it cannot be loaded or no
+CUDA device is present, `Engine()` raises `EngineUnavailable`. There is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .lower import Lowered
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libfrontier_b200.so")
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA engine library is missing or no B200 is visible."""
+
+
+class EngineError(RuntimeError):
+    """A call-level engine failure (CUDA error, bad arguments)."""
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the engine library (safe without a GPU: no CUDA call is made)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise EngineUnavailable(
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "fs_abi_version": (ctypes.c_int, []),
+        "fs_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(vp)]),
+        "fs_destroy": (None, [vp]),
+        "fs_last_error": (ctypes.c_char_p, [vp]),
+        "fs_last_launch_count": (ctypes.c_int, [vp]),
+        "fs_run_batch": (ctypes.c_int, [vp, vp, i32, vp, i32, vp, i32, vp, i64, abi.RequestSoA,
+                                        i64, vp, vp, abi.RequestOut, vp]),
+        "fs_stage": (ctypes.c_int, [vp, vp, i32, vp, i32, vp, i32, vp, i64, abi.RequestSoA, i64]),
+        "fs_launch_async": (ctypes.c_int, [vp, vp]),
+        "fs_fetch": (ctypes.c_int, [vp, vp, vp, abi.RequestOut]),
+        "fs_attention_cost": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp, vp]),
+        "fs_attention_cost_dev": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp, vp, vp]),
+        "fs_attention_features": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp]),
+        "fs_attention_features_dev": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp, vp]),
+        "fs_route_uniform": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
+        "fs_router_seeds": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i32, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    abi.check_sizes(lib, "fs_struct_sizes")
+    if lib.fs_abi_version() != 1:
+        raise EngineUnavailable("ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+class _AttnParamsC(ctypes.Structure):
+    _fields_ = [("num_query_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("dtype_bytes", ctypes.c_int32),
+                ("peak_flops", ctypes.c_double), ("mem_bw", ctypes.c_double),
+                ("kernel_overhead_us", ctypes.c_double)]
+
+
+def attn_params(num_query_heads, num_kv_heads, head_dim, dtype_bytes, peak_flops, mem_bw,
+                kernel_overhead_us=5.0) -> _AttnParamsC:
+    return _AttnParamsC(num_query_heads, num_kv_heads, head_dim, dtype_bytes, peak_flops, mem_bw,
+                        kernel_overhead_us)
+
+
+@dataclass
+class LogSpec:
+    """Per-instance capacities of the optional batch / routing log."""
+
+    batch_cap: int = 0
+    member_cap: int = 0
+    moe_cap: int = 0
+    route_cap: int = 0
+    counts_cap: int = 0
+
+
+@dataclass
+class RawLog:
+    spec: LogSpec
+    batches: np.ndarray
+    members: np.ndarray
+    moe: np.ndarray
+    routes: np.ndarray
+    counts: np.ndarray
+    batch_count: np.ndarray
+    route_count: np.ndarray
+    truncated: np.ndarray
+    c_struct: abi.LogC
+
+    def instance_batches(self, i: int) -> list[dict]:
+        s = self.spec
+        out = []
+        for j in range(int(self.batch_count[i])):
+            b = self.batches[i * s.batch_cap + j]
+            mo = int(b["member_offset"])
+            mem = self.members[i * s.member_cap + mo: i * s.member_cap + mo + int(b["n_members"])]
+            moe = None
+            if b["n_moe"] > 0:
+                eo = i * s.moe_cap + int(b["moe_offset"])
+                moe = self.moe[eo: eo + int(b["n_moe"])].tolist()
+            out.append({"replica": int(b["replica"]), "phase": abi.PHASES[int(b["phase"])],
+                        "t_complete": int(b["t_complete"]), "duration_ns": int(b["duration_ns"]),
+                        "members": mem.tolist(), "moe_ratio": moe})
+        return out
+
+    def instance_routes(self, i: int) -> list[dict]:
+        s = self.spec
+        out = []
+        for j in range(int(self.route_count[i])):
+            r = self.routes[i * s.route_cap + j]
+            co = i * s.counts_cap + int(r["counts_offset"])
+            out.append({"replica": int(r["replica"]), "micro_batch": int(r["micro_batch"]),
+                        "step": int(r["step"]), "layer": int(r["layer"]),
+                        "tokens": int(r["tokens"]),
+                        "counts": self.counts[co: co + int(r["n_experts"])].tolist()})
+        return out
+
+
+def make_log(n_instances: int, spec: LogSpec) -> RawLog:
+    def bases(cap):
+        return np.arange(n_instances, dtype=np.int64) * cap
+    log = RawLog(
+        spec=spec,
+        batches=np.zeros(max(1, n_instances * spec.batch_cap), dtype=abi.BATCH_REC),
+        members=np.zeros(max(1, n_instances * spec.member_cap), dtype=np.int32),
+        moe=np.zeros(max(1, n_instances * spec.moe_cap), dtype=np.float64),
+        routes=np.zeros(max(1, n_instances * spec.route_cap), dtype=abi.ROUTE_REC),
+        counts=np.zeros(max(1, n_instances * spec.counts_cap), dtype=np.int32),
+        batch_count=np.zeros(n_instances, dtype=np.int32),
+        route_count=np.zeros(n_instances, dtype=np.int32),
+        truncated=np.zeros(n_instances, dtype=np.int32),
+        c_struct=abi.LogC())
+    c = log.c_struct
+    log._keep = [bases(spec.batch_cap), bases(spec.member_cap), bases(spec.moe_cap),
+                 bases(spec.route_cap), bases(spec.counts_cap)]
+    c.batch_base, c.member_base, c.moe_base, c.route_base, c.counts_base = [
+        abi.ptr(b) for b in log._keep]
+    c.batch_cap, c.member_cap, c.moe_cap = spec.batch_cap, spec.member_cap, spec.moe_cap
+    c.route_cap, c.counts_cap = spec.route_cap, spec.counts_cap
+    c.batches = abi.ptr(log.batches) if spec.batch_cap else None
+    c.members = abi.ptr(log.members) if spec.member_cap else None
+    c.moe_ratio = abi.ptr(log.moe) if spec.moe_cap else None
+    c.routes = abi.ptr(log.routes) if spec.route_cap else None
+    c.counts = abi.ptr(log.counts) if spec.counts_cap else None
+    c.batch_count = abi.ptr(log.batch_count)
+    c.route_count = abi.ptr(log.route_count)
+    c.truncated = abi.ptr(log.truncated)
+    return log
+
+
+@dataclass
+class RawResults:
+    rows: np.ndarray
+    replica_out: np.ndarray
+    first_ns: np.ndarray
+    done_ns: np.ndarray
+    done_rank: np.ndarray
+    log: RawLog | None = None
+
+
+def alloc_results(low: Lowered) -> RawResults:
+    n = low.n_requests
+    return RawResults(rows=np.zeros(low.n_instances, dtype=abi.METRIC_ROW),
+                      replica_out=np.zeros(max(1, len(low.replicas)), dtype=abi.REPLICA_OUT),
+                      first_ns=np.zeros(max(1, n), dtype=np.int64),
+                      done_ns=np.zeros(max(1, n), dtype=np.int64),
+                      done_rank=np.zeros(max(1, n), dtype=np.int32))
+
+
+def soa(low: Lowered) -> abi.RequestSoA:
+    return abi.RequestSoA(abi.ptr(low.arrival), abi.ptr(low.prompt), abi.ptr(low.output),
+                          abi.ptr(low.id_rank))
+
+
+class Engine:
+    """One engine handle on one CUDA device."""
+
+    def __init__(self, device: int = 0) -> None:
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        rc = self.lib.fs_create(device, ctypes.byref(h))
+        if rc != 0:
+            raise EngineUnavailable(f"fs_create(device={device}) failed with code {rc} "
+                                    "(no CUDA device visible?)")
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.fs_destroy(self.h)
+            self.h = None
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str) -> None:
+        if rc != 0:
+            msg = self.lib.fs_last_error(self.h)
+            raise EngineError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self.lib.fs_last_launch_count(self.h))
+
+    # -- batched simulation -------------------------------------------------------------
+    def run(self, low: Lowered, log: LogSpec | None = None) -> RawResults:
+        res = alloc_results(low)
+        if log is not None:
+            res.log = make_log(low.n_instances, log)
+        pr = abi.RequestOut(abi.ptr(res.first_ns), abi.ptr(res.done_ns), abi.ptr(res.done_rank))
+        rc = self.lib.fs_run_batch(
+            self.h, abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas), len(low.replicas),
+            abi.ptr(low.prefixes), len(low.prefixes), abi.ptr(low.trace_counts),
+            len(low.trace_counts), soa(low), low.n_requests, abi.ptr(res.rows),
+            abi.ptr(res.replica_out), pr,
+            ctypes.byref(res.log.c_struct) if res.log is not None else None)
+        self._check(rc, "fs_run_batch")
+        return res
+
+    def stage(self, low: Lowered) -> None:
+        rc = self.lib.fs_stage(
+            self.h, abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas), len(low.replicas),
+            abi.ptr(low.prefixes), len(low.prefixes), abi.ptr(low.trace_counts),
+            len(low.trace_counts), soa(low), low.n_requests)
+        self._check(rc, "fs_stage")
+        self._staged = low
+
+    def launch(self, stream_ptr: int | None = None) -> None:
+        self._check(self.lib.fs_launch_async(self.h, stream_ptr), "fs_launch_async")
+
+    def fetch(self, low: Lowered | None = None, per_request: bool = True) -> RawResults:
+        low = low or self._staged
+        res = alloc_results(low)
+        pr = abi.RequestOut(abi.ptr(res.first_ns) if per_request else None,
+                            abi.ptr(res.done_ns) if per_request else None,
+                            abi.ptr(res.done_rank) if per_request else None)
+        self._check(self.lib.fs_fetch(self.h, abi.ptr(res.rows), abi.ptr(res.replica_out), pr),
+                    "fs_fetch")
+        return res
+
+    # -- cost-model kernels ----------------------------------------------------------------
+    def attention_cost(self, q, kv, offsets, is_decode, params) -> tuple[np.ndarray, np.ndarray]:
+        q = np.ascontiguousarray(q, dtype=np.int32)
+        kv = np.ascontiguousarray(kv, dtype=np.int32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        is_decode = np.ascontiguousarray(is_decode, dtype=np.uint8)
+        nb = len(offsets) - 1
+        out = np.zeros(max(nb, 1), dtype=np.float64)
+        st = np.zeros(max(nb, 1), dtype=np.int32)
+        self._check(self.lib.fs_attention_cost(self.h, abi.ptr(q), abi.ptr(kv), abi.ptr(offsets),
+                                               abi.ptr(is_decode), nb, params, abi.ptr(out),
+                                               abi.ptr(st)), "fs_attention_cost")
+        return out[:nb], st[:nb]
+
+    def attention_cost_dev(self, q_ptr, kv_ptr, off_ptr, dec_ptr, nb, params, out_ptr,
+                           status_ptr, stream_ptr) -> None:
+        self._check(self.lib.fs_attention_cost_dev(self.h, q_ptr, kv_ptr, off_ptr, dec_ptr, nb,
+                                                   params, out_ptr, status_ptr, stream_ptr),
+                    "fs_attention_cost_dev")
+
+    def attention_features(self, q, kv, offsets, is_decode, params) -> np.ndarray:
+        q = np.ascontiguousarray(q, dtype=np.int32)
+        kv = np.ascontiguousarray(kv, dtype=np.int32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        is_decode = np.ascontiguousarray(is_decode, dtype=np.uint8)
+        nb = len(offsets) - 1
+        out = np.zeros((max(nb, 1), 17), dtype=np.float64)
+        self._check(self.lib.fs_attention_features(self.h, abi.ptr(q), abi.ptr(kv),
+                                                   abi.ptr(offsets), abi.ptr(is_decode), nb,
+                                                   params, abi.ptr(out)), "fs_attention_features")
+        return out[:nb]
+
+    def route_uniform(self, tokens, seeds, num_experts: int, top_k: int):
+        tokens = np.ascontiguousarray(tokens, dtype=np.int64)
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        n = len(tokens)
+        counts = np.zeros((max(n, 1), num_experts), dtype=np.int32)
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        self._check(self.lib.fs_route_uniform(self.h, abi.ptr(tokens), abi.ptr(seeds), n,
+                                              num_experts, top_k, abi.ptr(counts), abi.ptr(st)),
+                    "fs_route_uniform")
+        return counts[:n], st[:n]
+
+    def router_seeds(self, prefixes: list[str], prefix_idx, micro_batch, steps, layers):
+        from .lower import _prefix
+        pf = np.array([_prefix(p) for p in prefixes], dtype=abi.SEED_PREFIX)
+        pidx = np.ascontiguousarray(prefix_idx, dtype=np.int32)
+        mb = np.ascontiguousarray(micro_batch, dtype=np.int32)
+        st = np.ascontiguousarray(steps, dtype=np.int64)
+        ly = np.ascontiguousarray(layers, dtype=np.int32)
+        out = np.zeros(max(len(pidx), 1), dtype=np.uint32)
+        self._check(self.lib.fs_router_seeds(self.h, abi.ptr(pf), abi.ptr(pidx), abi.ptr(mb),
+                                             abi.ptr(st), abi.ptr(ly), len(pidx), abi.ptr(out)),
+                    "fs_router_seeds")
+        return out[: len(pidx)]
+
+
+_default_engine: Engine | None = None
+
+
+def default_engine() -> Engine:
+    global _default_engine
+    if _default_engine is None:
+        import os as _os
+        dev = int(_os.environ.get("LOCAL_RANK", "0"))
+        _default_engine = Engine(dev)
+    return _default_engine
