@@ -1,0 +1,116 @@
+"""Device engine parity: CUDA path vs golden fixtures and vs the C oracle.
+
+Bit-exact for integer state (batch composition, expert counts, completion
+order, event counts) and for every fp64 latency/percentile (the engine
+reproduces Python's operation order; tolerance 0).
+"""
+
+import copy
+
+import numpy as np
+import pytest
+
+from parity import compare_to_golden, run_backend
+from paper_2508_03148_b200 import workloads as W
+from paper_2508_03148_b200.api import instance_spec
+from paper_2508_03148_b200.config import parse_config
+from paper_2508_03148_b200.lower import lower
+
+pytestmark = pytest.mark.gpu
+
+ROW_FIELDS = ("status", "iterations", "events", "total_tokens", "makespan_ns", "prefill_batches",
+              "decode_batches", "af_steps", "n_tpot", "makespan_s",
+              "throughput_tokens_per_s_per_gpu", "ttft", "tpot", "e2e", "avg_input_tokens",
+              "avg_output_tokens", "af_busy_ns", "af_busy_fraction", "routing_calls")
+
+
+def assert_same_raw(dev, ref):
+    assert (dev.first_ns == ref.first_ns).all()
+    assert (dev.done_ns == ref.done_ns).all()
+    assert (dev.done_rank == ref.done_rank).all()
+    for f in ROW_FIELDS:
+        a, b = dev.rows[f], ref.rows[f]
+        same = (a == b) | (np.isnan(a) & np.isnan(b)) if a.dtype.kind == "f" else (a == b)
+        assert np.all(same), f
+    bf_a, bf_b = dev.rows["bubble_fraction"], ref.rows["bubble_fraction"]
+    assert np.all((bf_a == bf_b) | (np.isnan(bf_a) & np.isnan(bf_b)))
+    assert (dev.replica_out["busy_ns"] == ref.replica_out["busy_ns"]).all()
+    assert (dev.replica_out["steps_executed"] == ref.replica_out["steps_executed"]).all()
+
+
+def test_scenarios_vs_golden(engine, golden_scenarios):
+    names = list(golden_scenarios)
+    res = run_backend(engine, [golden_scenarios[n]["config"] for n in names], routes=True)
+    failures = {n: compare_to_golden(r, golden_scenarios[n]) for n, r in zip(names, res)}
+    assert {n: b for n, b in failures.items() if b} == {}
+
+
+@pytest.mark.parametrize("name", ["C1_colocated_llama7b_1000", "C3_pd_70b_tight_300",
+                                  "C3_pd_70b_roomy_300", "C4_af_dsv3_10", "C4_colocated_ep8_10"])
+def test_baseline_configs_vs_golden(engine, golden_baseline, name):
+    g = golden_baseline[name]
+    r = run_backend(engine, [g["config"]], routes=name.startswith("C4"))[0]
+    assert compare_to_golden(r, g) == []
+
+
+def test_c5_design_points_vs_golden(engine, golden_c5):
+    base = W.c5_sweep_configs(64)
+    docs = []
+    for ci in range(64):
+        d = copy.deepcopy(base[ci])
+        d["seed"] = 1000 + 64 * ci
+        docs.append(d)
+    res = run_backend(engine, docs)
+    bad = {ci: compare_to_golden(r, golden_c5[str(ci)]) for ci, r in enumerate(res)}
+    assert {k: v for k, v in bad.items() if v} == {}
+
+
+def test_full_c5_sweep_vs_oracle(engine):
+    """All 64 configs x 8 seeds: device == oracle on every output array."""
+    from oracle import oracle
+    docs = W.c5_sweep(n_seeds=8)
+    low = lower([instance_spec(parse_config(d)) for d in docs])
+    dev = engine.run(low)
+    ref = oracle.run(low, threads=8)
+    assert_same_raw(dev, ref)
+
+
+def test_route_uniform_vectors(engine, golden_pure):
+    groups = {}
+    for T, E, k, seed, counts in golden_pure["route_uniform"]:
+        groups.setdefault((E, k), []).append((T, seed, counts))
+    for (E, k), calls in groups.items():
+        counts, st = engine.route_uniform([c[0] for c in calls], [c[1] for c in calls], E, k)
+        assert (st == 0).all()
+        assert counts.tolist() == [c[2] for c in calls]
+
+
+def test_router_seed_vectors(engine, golden_pure):
+    rows = golden_pure["router_seed"]
+    prefixes = [f"{m}:{s}:" for m, s, _, _, _ in rows]
+    got = engine.router_seeds(prefixes, list(range(len(rows))), [0] * len(rows),
+                              [r[2] for r in rows], [r[3] for r in rows])
+    assert got.tolist() == [r[4] for r in rows]
+
+
+def test_attention_cost_vectors(engine, golden_pure):
+    from paper_2508_03148_b200.engine import attn_params
+    for phase, q, kv, hq, hkv, hd, us, vec in golden_pure["attention"]:
+        off = np.array([0, len(q)], dtype=np.int64)
+        p = attn_params(hq, hkv, hd, 2, 2.25e15, 8e12, 5.0)
+        out, st = engine.attention_cost(q, kv, off, [phase == "decode"], p)
+        assert st[0] == 0 and out[0] == us
+        feats = engine.attention_features(q, kv, off, [phase == "decode"], p)
+        assert feats[0].tolist() == vec
+
+
+def test_attention_cost_bulk_vs_oracle(engine):
+    from oracle import oracle
+    from paper_2508_03148_b200.engine import attn_params
+    q, kv, off, dec = W.attention_batches(4096)
+    p = attn_params(32, 8, 128, 2, 2.25e15, 8e12, 5.0)
+    out, st = engine.attention_cost(q, kv, off, dec, p)
+    assert (st == 0).all()
+    for b in range(0, 4096, 97):
+        s, e = off[b], off[b + 1]
+        assert out[b] == oracle.attention_us(bool(dec[b]), q[s:e], kv[s:e], 32, 8, 128, 2.25e15, 8e12)
