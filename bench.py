@@ -1,0 +1,372 @@
+"""Benchmark: simulated iterations/s over the C5 config sweep (BASELINE.json metric).
+
+A *step* is one pass of the hot path over one batch of synthetic input: the
+whole 4,096-instance C5 design-space sweep (64 configs x 64 trace seeds, 64
+requests each: SURVEY.md section 8(d)) simulated to completion on the GPU,
+metric rows included. An *iteration* is one BATCH_COMPLETE event (prefill
+batch, decode step or AF step), counted by the engine.
+
+  value  device-resident inputs (fs_stage once, fs_launch_async per step),
+         CUDA events on the launch stream, L2 flushed between steps (outside
+         the events), max over ranks; whole-job iterations / time.
+  e2e    the drop-in C-ABI call fs_run_batch with HOST buffers each step:
+         H2D of descriptors + request SoA, both kernels, D2H of metric rows,
+         replica rows and per-request times, wall clock.
+
+Multi-GPU (torchrun): one process per GPU, each simulating its own 4,096
+instances (weak scaling; disjoint seeds), then one NCCL all-gather of the
+fixed-size metric rows. `--impl reference` times the CPU port of the
+reference path (oracle/fs_oracle.c, all host threads) on a bounded sample of
+the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated iterations/sec over config sweep"
+UNIT = "iterations/s"
+SEED_STRIDE = 1_000_000
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seeds", type=int, default=64, help="trace seeds per config (64 -> 4096)")
+    ap.add_argument("--requests", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-seeds", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_docs(rank: int, n_seeds: int, n_requests: int):
+    from paper_2508_03148_b200 import workloads as W
+    return W.c5_sweep(n_seeds=n_seeds, n_requests=n_requests, seed_base=1000 + SEED_STRIDE * rank)
+
+
+def lower_docs(docs):
+    from paper_2508_03148_b200.api import instance_spec
+    from paper_2508_03148_b200.config import parse_config
+    from paper_2508_03148_b200.lower import lower
+    return lower([instance_spec(parse_config(d)) for d in docs])
+
+
+def cpu_count() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_oracle_sample(n_requests: int, sample_seeds: int, threads: int, rank: int = 0):
+    """CPU port of the reference path on all 64 configs x `sample_seeds` seeds."""
+    from oracle import oracle
+    docs = workload_docs(rank, sample_seeds, n_requests)
+    low = lower_docs(docs)
+    oracle.load()
+    t0 = time.perf_counter()
+    res = oracle.run(low, threads=threads)
+    dt = time.perf_counter() - t0
+    its = int(res.rows["iterations"].sum())
+    return its, dt, len(docs)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def algorithmic_bytes(low, rows) -> int:
+    """SURVEY.md 8(d) DES-step bytes: 16 B per batch membership (a member's
+    context and remaining-token counters read + written) plus one read of the
+    instance inputs and one write of its outputs."""
+    import numpy as np
+    memberships = int(rows["total_tokens"].sum())  # each membership emits exactly one token
+    n_req = low.n_requests
+    inputs = (low.descs.nbytes + low.replicas.nbytes + low.prefixes.nbytes
+              + n_req * (8 + 4 + 4 + 4))
+    outputs = rows.nbytes + n_req * (8 + 8 + 4)
+    return 16 * memberships + inputs + outputs + 0 * int(np.int64(0))
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    if world != args.gpus and args.gpus != 1:
+        pass  # trust WORLD_SIZE when launched by torchrun
+    if args.impl == "reference":
+        return main_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2508_03148_b200 import abi
+    from paper_2508_03148_b200.engine import Engine
+
+    t_low0 = time.perf_counter()
+    docs = workload_docs(rank, args.seeds, args.requests)
+    low = lower_docs(docs)
+    t_low = time.perf_counter() - t_low0
+    eng = Engine(local)
+    stream = torch.cuda.Stream(device=local)
+    eng.stage(low)
+    flush = torch.empty(int(256 * 2**20) // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    # warm-up (also validates every instance ran)
+    for _ in range(max(args.warmup, 1)):
+        eng.launch(stream.cuda_stream)
+    torch.cuda.synchronize()
+    res = eng.fetch(low, per_request=False)
+    if (res.rows["status"] != 0).any():
+        bad = int((res.rows["status"] != 0).sum())
+        raise SystemExit(f"{bad} instances failed: statuses {np.unique(res.rows['status'])}")
+    iters_per_step = int(res.rows["iterations"].sum())
+    launches_per_step = eng.last_launch_count
+
+    # timed region: device-resident inputs
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.zero_()  # > L2 (126 MB): evict the previous step's state
+                starts[i].record(stream)
+                eng.launch(stream.cuda_stream)
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    its = torch.tensor([iters_per_step * args.steps], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(its, op=dist.ReduceOp.SUM)
+    max_ms = float(t.item())
+    total_its = float(its.item())
+    value = total_its / (max_ms / 1e3)
+
+    # kernel share: time the simulation kernel alone vs the metrics kernel
+    # (events around each phase of one extra launch are not possible inside the
+    # library; the ncu launch list in profiles/ gives the split).
+
+    # end-to-end through the C ABI with host buffers (H2D + kernels + D2H)
+    e2e_times = []
+    raw = None
+    for i in range(args.warmup + args.steps):
+        if world > 1 and i == args.warmup:
+            dist.barrier()
+        t0 = time.perf_counter()
+        raw = eng.run(low)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = total_its / float(e2e_s.item())
+    h2d = (low.descs.nbytes + low.replicas.nbytes + low.prefixes.nbytes + low.trace_counts.nbytes
+           + low.arrival.nbytes + low.prompt.nbytes + low.output.nbytes + low.id_rank.nbytes)
+    d2h = (raw.rows.nbytes + raw.replica_out.nbytes + raw.first_ns.nbytes + raw.done_ns.nbytes
+           + raw.done_rank.nbytes)
+    assert (raw.rows["iterations"] == res.rows["iterations"]).all()
+
+    # the only collective: gather every rank's fixed-size metric rows (NCCL)
+    gather_ms = None
+    if world > 1:
+        rows_t = torch.from_numpy(raw.rows.view(np.uint8).copy()).to(f"cuda:{local}")
+        out = [torch.empty_like(rows_t) for _ in range(world)]
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        dist.all_gather(out, rows_t)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - g0) * 1e3
+
+    # roofline of the dominant kernel (the DES step kernel)
+    alg_bytes = algorithmic_bytes(low, res.rows)
+    peak, peak_kind = measured_peaks()
+    avg_ms = max_ms / args.steps
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    traffic = ncu_traffic("sim_kernel")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_count()
+        c_its, c_dt, n_inst = run_oracle_sample(args.requests, args.cpu_sample_seeds, threads)
+        cpu = {"value": c_its / c_dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"C5 configs x {args.cpu_sample_seeds} seeds = {n_inst} instances "
+                         f"({c_its} iterations) in {c_dt:.2f}s on {threads} threads "
+                         f"({cpu_model()}); oracle/fs_oracle.c"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64+int64", "data": "synthetic",
+            "config": {"workload": "C5 design-space sweep: 64 configs x "
+                                   f"{args.seeds} seeds x {args.requests} requests per GPU",
+                       "instances_per_gpu": low.n_instances, "iterations_per_step": iters_per_step * world,
+                       "parallelism": f"instances sharded over {world} GPU(s), NCCL gather of rows",
+                       "l2": "flushed between steps (256 MB write, outside events)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "host_lowering_s": t_low},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "sim_kernel (+metrics_kernel)",
+                         "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "gather_ms": gather_ms,
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main_reference(args, rank, world):
+    """CPU port of the reference path (oracle/fs_oracle.c) with every host thread."""
+    if rank != 0:
+        return
+    threads = cpu_count()
+    from oracle import oracle
+    docs = workload_docs(0, args.cpu_sample_seeds, args.requests)
+    low = lower_docs(docs)
+    oracle.load()
+    times = []
+    its = 0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = oracle.run(low, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            its = int(res.rows["iterations"].sum())
+    value = its * len(times) / sum(times)
+    sample = (f"C5 configs x {args.cpu_sample_seeds} seeds = {low.n_instances} instances "
+              f"({its} iterations) per step on {threads} threads ({cpu_model()})")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / len(times) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64+int64", "data": "synthetic",
+            "config": {"workload": f"C5 design-space sweep: 64 configs x {args.seeds} seeds x "
+                                   f"{args.requests} requests per GPU (timed on a "
+                                   f"{args.cpu_sample_seeds}-seed sample)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

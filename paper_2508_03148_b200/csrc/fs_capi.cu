@@ -45,7 +45,7 @@ struct fs_engine {
   DevBuf descs, reps, prefixes, mid, trace, arrival, prompt, output, id_rank, order;
   // workspace
   DevBuf first, done, rank, finish, home, lists, list_base, heap, heap_base, xfer, rstate, af_ffn,
-      af_base, work;
+      af_base, work, cycles;
   // outputs
   DevBuf rows, rep_out;
   // log mirrors
@@ -123,6 +123,14 @@ const char* fs_last_error(const fs_engine* e) { return e ? e->err.c_str() : "nul
 
 int fs_last_launch_count(const fs_engine* e) { return e ? e->last_launches : 0; }
 
+// SM cycles each instance of the last launch took (profiling aid)
+int fs_instance_cycles(fs_engine* e, int64_t* out) {
+  if (!e || !e->staged) return 1;
+  FS_CHECK(cudaDeviceSynchronize());
+  FS_CHECK(cudaMemcpy(out, e->cycles.p, 8 * (size_t)e->n_inst, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
              const fs_replica_desc* replicas, int32_t n_replicas, const fs_seed_prefix* prefixes,
              int32_t n_prefixes, const int64_t* trace_counts, int64_t n_trace_counts,
@@ -192,6 +200,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   FS_CHECK(e->rstate.ensure((size_t)std::max(n_replicas, 1) * sizeof(RepState)));
   FS_CHECK(e->af_ffn.ensure((size_t)std::max<int64_t>(ab, 1) * 8));
   FS_CHECK(e->work.ensure(sizeof(int32_t)));
+  FS_CHECK(e->cycles.ensure((size_t)std::max(n_instances, 1) * 8));
   FS_CHECK(e->rows.ensure((size_t)std::max(n_instances, 1) * sizeof(fs_metric_row)));
   FS_CHECK(e->rep_out.ensure((size_t)std::max(n_replicas, 1) * sizeof(fs_replica_out)));
   // done_ns / first_ns start at -1 so a request the engine never reached is visible
@@ -228,6 +237,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   P.rows = e->rows.as<fs_metric_row>();
   P.rep_out = e->rep_out.as<fs_replica_out>();
   P.work_counter = e->work.as<int32_t>();
+  P.inst_cycles = e->cycles.as<int64_t>();
   P.log_enabled = 0;
   e->n_inst = n_instances;
   e->n_reps = n_replicas;

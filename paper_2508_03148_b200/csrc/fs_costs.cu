@@ -175,7 +175,7 @@ __global__ void attention_features_kernel(const int32_t* q, const int32_t* kv, c
       }
       s = warp_sum_i64(s);
       s2 = warp_sum_i64(s2);
-      mx = -warp_min_i64(-mx);
+      mx = warp_max_i64(mx);
       mn = warp_min_i64(mn);
       // integer-valued sums below 2^53 are exact in any summation order
       const double sum = i2d(s);

@@ -332,30 +332,34 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
 }
 
 // ---- optional batch log -------------------------------------------------------------------
-__device__ double* log_moe_slot(const EngineParams& P, const Inst& I) {
-  if (!P.log_enabled || !P.log.batches || !I.d->has_moe) return nullptr;
-  if (I.log_eoff + I.d->num_layers > P.log.moe_cap) return nullptr;
-  return P.log.moe_ratio + P.log.moe_base[I.idx] + I.log_eoff;
+// A batch's moe-ratio slot is reserved when it starts: several replicas can have
+// batches in flight, so slots are handed out in start order and each batch
+// record points at its own. Returns offset + 1 (0 = not logged).
+__device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
+  if (!P.log_enabled || !P.log.batches || !I.d->has_moe) return 0;
+  if (I.log_eoff + I.d->num_layers > P.log.moe_cap) return 0;
+  const int32_t off = I.log_eoff;
+  I.log_eoff += I.d->num_layers;
+  return off + 1;
 }
 __device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
-                          const int32_t* members, int nm, bool moe_slot) {
+                          const int32_t* members, int nm, int32_t moe_off1) {
   if (!P.log_enabled || !P.log.batches) return;
-  const int n_moe = moe_slot ? I.d->num_layers : 0;
+  const int n_moe = moe_off1 ? I.d->num_layers : 0;
   const bool need_moe = I.d->has_moe && phase != PH_AF;
   const int32_t c = I.log_batches;
-  if (c < P.log.batch_cap && I.log_moff + nm <= P.log.member_cap && (!need_moe || moe_slot)) {
+  if (c < P.log.batch_cap && I.log_moff + nm <= P.log.member_cap && (!need_moe || moe_off1)) {
     if (I.lane == 0) {
       fs_batch_rec rec;
       rec.replica = r; rec.phase = phase; rec.t_complete = I.now; rec.duration_ns = dur;
       rec.n_members = nm; rec.member_offset = I.log_moff;
-      rec.moe_offset = n_moe ? I.log_eoff : -1;
+      rec.moe_offset = n_moe ? moe_off1 - 1 : -1;
       rec.n_moe = n_moe;
       P.log.batches[P.log.batch_base[I.idx] + c] = rec;
     }
     const int64_t mb = P.log.member_base[I.idx] + I.log_moff;
     for (int i = I.lane; i < nm; i += 32) P.log.members[mb + i] = members[i];
     I.log_moff += nm;
-    I.log_eoff += n_moe;
     I.log_batches = c + 1;
   } else if (I.lane == 0) {
     P.log.truncated[I.idx] = 1;
@@ -524,7 +528,8 @@ __device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& 
 __device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, const BatchShape& b, int phase,
                              WarpSmem* sm) {
-  double* moe_slot = log_moe_slot(P, I);
+  const int32_t moe_off1 = log_moe_reserve(P, I);
+  double* moe_slot = moe_off1 ? P.log.moe_ratio + P.log.moe_base[I.idx] + (moe_off1 - 1) : nullptr;
   const double us = execute_batch(P, I, r, rd, b, s.steps, sm, moe_slot);
   if (I.status) return;
   const int64_t dur = py_round(us * 1000.0);
@@ -532,7 +537,7 @@ __device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
   s.steps++;
   s.inflight_phase = phase;
   s.inflight_dur = dur;
-  s.inflight_moe = moe_slot != nullptr;
+  s.inflight_moe = moe_off1;
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
 }
 
@@ -1013,6 +1018,7 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
 
 // ---- the per-instance event loop -------------------------------------------------------------------
 __device__ void simulate_instance(const EngineParams& P, int idx, int lane, WarpSmem* sm) {
+  const long long t_start = clock64();
   Inst I;
   const fs_instance_desc* d = &P.descs[idx];
   I.d = d;
@@ -1102,6 +1108,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, Warp
       if (P.log.batch_count) P.log.batch_count[idx] = I.log_batches;
       if (P.log.route_count) P.log.route_count[idx] = I.log_routes;
     }
+    if (P.inst_cycles) P.inst_cycles[idx] = clock64() - t_start;
   }
   for (int r = lane; r < I.R; r += 32) {
     const RepState s = P.rstate[I.rb + r];

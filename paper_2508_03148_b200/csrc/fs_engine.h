@@ -66,6 +66,7 @@ struct EngineParams {
   fs_log log;
   int32_t log_enabled;
   int32_t* work_counter;
+  int64_t* inst_cycles;          // SM cycles each instance took (profiling aid)
 };
 
 // host-side launchers (fs_engine.cu / fs_metrics.cu / fs_costs.cu)

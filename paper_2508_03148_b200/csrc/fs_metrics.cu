@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(32 * kMetricWarps) metrics_kernel(EngineParams
       }
       ntp += __popc(tm);
     }
-    maxdone = -warp_min_i64(-maxdone);
+    maxdone = warp_max_i64(maxdone);
     minarr = warp_min_i64(minarr);
     sum_p = warp_sum_i64(sum_p);
     sum_o = warp_sum_i64(sum_o);
