@@ -45,7 +45,7 @@ struct fs_engine {
   DevBuf descs, reps, prefixes, mid, trace, arrival, prompt, output, id_rank, order;
   // workspace
   DevBuf first, done, rank, finish, home, lists, list_base, heap, heap_base, xfer, rstate, af_ffn,
-      af_base, work, cycles;
+      af_base, work, cycles, jobs, job_counts, inst_done;
   // outputs
   DevBuf rows, rep_out;
   // log mirrors
@@ -239,6 +239,23 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   P.work_counter = e->work.as<int32_t>();
   P.inst_cycles = e->cycles.as<int64_t>();
   P.log_enabled = 0;
+  // routing job board: one slot per resident warp of the persistent grid
+  P.n_slots = fs::simulation_slots(e->n_sms, n_instances);
+  int max_e = 0;
+  for (int i = 0; i < n_instances; i++)
+    if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);
+  P.job_max_e = std::min(max_e, FS_MAX_EXPERTS);
+  FS_CHECK(e->inst_done.ensure(sizeof(int32_t)));
+  P.inst_done = e->inst_done.as<int32_t>();
+  if (max_e > 0) {
+    FS_CHECK(e->jobs.ensure((size_t)P.n_slots * sizeof(fs::RouteJob)));
+    FS_CHECK(e->job_counts.ensure((size_t)P.n_slots * fs::kJobLayers * P.job_max_e * 4));
+    P.jobs = e->jobs.as<fs::RouteJob>();
+    P.job_counts = e->job_counts.as<int32_t>();
+  } else {
+    P.jobs = nullptr;
+    P.job_counts = nullptr;
+  }
   e->n_inst = n_instances;
   e->n_reps = n_replicas;
   e->n_prefixes = n_prefixes;
@@ -254,6 +271,9 @@ int fs_launch_async(fs_engine* e, void* stream) {
   if (!e || !e->staged) return 1;
   cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
   FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
+  FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, sizeof(int32_t), s));
+  if (e->params.jobs)
+    FS_CHECK(cudaMemsetAsync(e->jobs.p, 0, (size_t)e->params.n_slots * sizeof(fs::RouteJob), s));
   e->last_launches = 0;
   e->last_launches += fs::launch_simulation(e->params, e->n_sms, s);
   e->last_launches += fs::launch_metrics(e->params, s);

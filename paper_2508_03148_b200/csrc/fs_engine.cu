@@ -58,7 +58,7 @@ struct __align__(16) WarpSmem {
 
 struct Inst {
   const fs_instance_desc* d;
-  int idx, N, R, mode, lane;
+  int idx, N, R, mode, lane, slot;
   int64_t ro;      // request offset (global index of local request 0)
   int rb;          // global index of local replica 0
   int32_t* lists;  // 3*N ints per replica: queue, running, inflight members
@@ -270,6 +270,218 @@ __device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t
   __syncwarp();
 }
 
+// ---- routing job board -----------------------------------------------------------------------
+// One batch's uniform router calls (up to kJobLayers layers x T tokens x E
+// experts of Philox draws) dwarf everything else an MoE instance does, and a
+// sweep's MoE instances are its longest. So the owning warp publishes the
+// calls as a job of row chunks on a GPU-wide board; it works on its own job,
+// and every warp whose share of the instance queue is exhausted scans the
+// board and claims chunks of other warps' jobs. A claimed chunk pins its job
+// (the job cannot complete, hence cannot be replaced, until the chunk's
+// completion is counted), so chunk parameters are stable for the claimant.
+// Counts land in the job's global tally with warp-aggregated atomics; the owner
+// waits for every chunk, fences, and reads the tally through L2.
+constexpr unsigned kChunkBits = 20;
+constexpr unsigned long long kChunkMask = (1ull << kChunkBits) - 1;
+constexpr int kMaxChunks = 1 << 18;
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
+  return *reinterpret_cast<const volatile int32_t*>(p);
+}
+
+// returns a claimed chunk index or -1 (same on all lanes)
+__device__ int claim_chunk(RouteJob* job, int lane) {
+  long long c = -1;
+  if (lane == 0) {
+    const unsigned long long v = ld_volatile_u64(&job->ctr);
+    if ((v & kChunkMask) < ((v >> kChunkBits) & kChunkMask)) {
+      const unsigned long long old = atomicAdd(&job->ctr, 1ull);
+      if ((old & kChunkMask) < ((old >> kChunkBits) & kChunkMask)) c = (long long)(old & kChunkMask);
+    }
+  }
+  c = __shfl_sync(FS_FULL, c, 0);
+  if (c >= 0) __threadfence();
+  return (int)c;
+}
+
+template <int KCAP>
+__device__ void process_chunk_k(RouteJob* job, int32_t* counts, int c, int lane) {
+  const int64_t T = __ldcg(&job->T);
+  const int E = __ldcg(&job->E), k = __ldcg(&job->k), nl = __ldcg(&job->nl);
+  const int nseg = __ldcg(&job->nseg), ppc = __ldcg(&job->passes_per_chunk);
+  const int rows_per_pass = 32 / nseg;
+  const int seg_len = (E + nseg - 1) / nseg;
+  const int64_t total_rows = (int64_t)nl * T;
+  const int kc = k + 1;
+  const int seg = lane % nseg;
+  int tie = 0;
+  for (int p = 0; p < ppc; p++) {
+    const int64_t pass_row0 = ((int64_t)c * ppc + p) * rows_per_pass;
+    if (pass_row0 >= total_rows) break;
+    const int64_t row_j = pass_row0 + lane / nseg;
+    const bool active = row_j < total_rows;
+    uint64_t top[KCAP];
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) top[j] = ~0ull;
+    uint64_t thr = ~0ull;
+    int layer = 0;
+    if (active) {
+      layer = (int)(row_j / T);
+      const int64_t r = row_j - (int64_t)layer * T;
+      const uint64_t k0 = __ldcg(&job->keys[layer][0]), k1 = __ldcg(&job->keys[layer][1]);
+      const int e0 = seg * seg_len, e1 = min(E, e0 + seg_len);
+      const uint64_t rb = (uint64_t)r * (uint64_t)E;
+      if (e0 < e1) topk_scan<KCAP>(top, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+    }
+    for (int s = 1; s < nseg; s <<= 1) {
+      uint64_t other[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, top[j], s);
+#pragma unroll
+      for (int j = 0; j < KCAP; j++)
+        if (j < kc) topk_insert<KCAP>(top, kc, other[j], thr);
+    }
+    const bool leader = active && seg == 0;
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) {
+      if (j < k) {
+        const int key = leader ? layer * E + (int)(top[j] & 0x7FF) : -1;
+        const unsigned grp = __match_any_sync(FS_FULL, key);
+        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counts[key], __popc(grp));
+      }
+      if (j == k && leader && ((top[j] >> 11) == (top[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
+    }
+  }
+  if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
+}
+
+__device__ void process_chunk(RouteJob* job, int32_t* counts, int c, int lane) {
+  const int k = __ldcg(&job->k);
+  if (k + 1 <= 4) process_chunk_k<4>(job, counts, c, lane);
+  else if (k + 1 <= 9) process_chunk_k<9>(job, counts, c, lane);
+  else process_chunk_k<FS_MAX_TOPK + 1>(job, counts, c, lane);
+  __threadfence();
+  if (lane == 0) atomicAdd(&job->done, 1);
+  __syncwarp();
+}
+
+__device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slot) {
+  return P.job_counts + (int64_t)slot * kJobLayers * P.job_max_e;
+}
+
+// Route layers [l0, l0+nl) of one batch; the tally of layer l0+j ends up at
+// job_counts_of(slot)[j*E ...]. Returns FS_OK or FS_ERR_ROUTING_TIE.
+__device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
+                             int l0, int nl, int64_t T) {
+  const fs_instance_desc* d = I.d;
+  RouteJob* job = &P.jobs[I.slot];
+  int32_t* counts = job_counts_of(P, I.slot);
+  const int E = d->num_experts, k = d->top_k;
+  // router seeds + Philox keys, one layer per lane (base.py:63-65, routing.py:59-62)
+  const int layer = l0 + I.lane;
+  if (I.lane < nl) {
+    const fs_seed_prefix* pf = &P.prefixes[prefix];
+    int64_t ints[3];
+    int n = 0;
+    if (mb > 0) ints[n++] = mb;
+    ints[n++] = step;
+    ints[n++] = layer;
+    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->len / 64,
+                                                 pf->bytes, pf->len, ints, n);
+    uint64_t key[2];
+    routing_key((uint64_t)seed, key);
+    job->keys[I.lane][0] = key[0];
+    job->keys[I.lane][1] = key[1];
+  }
+  for (int i = I.lane; i < nl * E; i += 32) counts[i] = 0;
+  // geometry: split rows into segments while there are few of them
+  const int64_t rows = (int64_t)nl * T;
+  int nseg = 1;
+  while (nseg < 32 && (nseg * 2) * 4 <= E && rows * nseg < 2048) nseg *= 2;
+  const int64_t passes = (rows + (32 / nseg) - 1) / (32 / nseg);
+  int ppc = (int)((passes + 1023) / 1024);
+  if (ppc < 1) ppc = 1;
+  int64_t n_chunks = (passes + ppc - 1) / ppc;
+  if (n_chunks > kMaxChunks) {
+    ppc = (int)((passes + kMaxChunks - 1) / kMaxChunks);
+    n_chunks = (passes + ppc - 1) / ppc;
+  }
+  if (I.lane == 0) {
+    job->T = T; job->E = E; job->k = k; job->nl = nl; job->nseg = nseg;
+    job->passes_per_chunk = ppc; job->done = 0; job->tie = 0;
+  }
+  __syncwarp();
+  __threadfence();
+  const bool shared = n_chunks > 2;  // tiny jobs are not worth publishing
+  if (I.lane == 0) {
+    const unsigned long long epoch =
+        ((ld_volatile_u64(&job->ctr) >> (2 * kChunkBits)) + 1) & 0xFFFFFFull;
+    const unsigned long long v = (epoch << (2 * kChunkBits)) |
+                                 ((unsigned long long)n_chunks << kChunkBits);
+    // a private job is published fully claimed, so helpers never see it
+    atomicExch(&job->ctr, shared ? v : (v | (unsigned long long)n_chunks));
+  }
+  __syncwarp();
+  if (shared) {
+    for (int c; (c = claim_chunk(job, I.lane)) >= 0;) process_chunk(job, counts, c, I.lane);
+    while (ld_volatile_i32(&job->done) < n_chunks) __nanosleep(64);
+  } else {
+    for (int c = 0; c < n_chunks; c++) process_chunk(job, counts, c, I.lane);
+  }
+  __threadfence();
+  __syncwarp();
+  return ld_volatile_i32(&job->tie) ? FS_ERR_ROUTING_TIE : FS_OK;
+}
+
+// uniform routing with real draws goes through the job board; the trace policy
+// and the RNG-free shortcuts (T == 0, top_k == E) stay on the owning warp
+__device__ __forceinline__ bool use_job_board(const fs_instance_desc* d, int policy, int64_t T) {
+  return policy == FS_ROUTE_UNIFORM && T > 0 && d->top_k < d->num_experts &&
+         d->top_k >= 1 && d->top_k <= FS_MAX_TOPK && d->num_experts <= FS_MAX_EXPERTS;
+}
+
+// copy one layer's tally from the job (through L2) to the warp's counts
+__device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, WarpSmem* sm) {
+  const int E = I.d->num_experts;
+  const int32_t* counts = job_counts_of(P, I.slot) + (int64_t)j * E;
+  __syncwarp();
+  for (int e = I.lane; e < E; e += 32) sm->counts[e] = __ldcg(counts + e);
+  __syncwarp();
+}
+
+// warps with no instance left help route other warps' jobs until every
+// instance has finished
+__device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
+  const int ns = P.n_slots;
+  const unsigned rot = (unsigned)my_slot * 2654435761u;
+  while (ld_volatile_i32(P.inst_done) < P.n_inst) {
+    bool found = false;
+    for (int base = 0; base < ns; base += 32) {
+      const int s = (int)((rot + (unsigned)(base + lane)) % (unsigned)ns);
+      bool avail = false;
+      if (base + lane < ns) {
+        const unsigned long long v = ld_volatile_u64(&P.jobs[s].ctr);
+        avail = (v & kChunkMask) < ((v >> kChunkBits) & kChunkMask);
+      }
+      unsigned m = __ballot_sync(FS_FULL, avail);
+      while (m) {
+        const int pick = __ffs(m) - 1;
+        m &= m - 1;
+        const int sp = __shfl_sync(FS_FULL, s, pick);
+        RouteJob* job = &P.jobs[sp];
+        for (int c; (c = claim_chunk(job, lane)) >= 0;) {
+          process_chunk(job, job_counts_of(P, sp), c, lane);
+          found = true;
+        }
+      }
+    }
+    if (!found) __nanosleep(256);
+  }
+}
+
 // ---- execute_batch (cluster.py:317-346) ---------------------------------------------------
 struct BatchShape {
   int64_t n_tokens, sum_q, sum_kv;
@@ -300,11 +512,19 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
     tot = tot + coll;
     for (int l = 0; l < L; l++) ls.add(tot);  // never L * tot: Python adds layer by layer
   } else {
+    const bool board = use_job_board(I.d, d->routing_policy, n);
     for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
-      derive_layer_keys(P, I, rd.prefix, 0, step, l0, L, sm);
       const int lend = min(L, l0 + kLayerChunk);
+      if (board) {
+        const int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n);
+        if (st != FS_OK) { fail(I, st, l0); return 0.0; }
+      } else {
+        derive_layer_keys(P, I, rd.prefix, 0, step, l0, L, sm);
+      }
       for (int l = l0; l < lend; l++) {
-        int st = route_layer(P, I, d->routing_policy, n, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
+        int st = FS_OK;
+        if (board) load_job_layer(P, I, l - l0, sm);
+        else st = route_layer(P, I, d->routing_policy, n, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
         if (st != FS_OK) { fail(I, st, l); return 0.0; }
         I.routing_calls++;
         log_route(P, I, r, 0, step, l, n, sm);
@@ -926,11 +1146,19 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
       const int64_t fns = py_round(f * 1000.0);
       for (int k = I.lane; k < L; k += 32) ffn[(int64_t)i * L + k] = fns;
     } else {
+      const bool board = use_job_board(d, FS_ROUTE_UNIFORM, sz);
       for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
-        derive_layer_keys(P, I, rd.prefix_mb, i + 1, step, l0, L, sm);
         const int lend = min(L, l0 + kLayerChunk);
+        if (board) {
+          const int st = run_route_job(P, I, rd.prefix_mb, i + 1, step, l0, lend - l0, sz);
+          if (st != FS_OK) { fail(I, st, l0); return; }
+        } else {
+          derive_layer_keys(P, I, rd.prefix_mb, i + 1, step, l0, L, sm);
+        }
         for (int l = l0; l < lend; l++) {
-          int st = route_layer(P, I, FS_ROUTE_UNIFORM, sz, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
+          int st = FS_OK;
+          if (board) load_job_layer(P, I, l - l0, sm);
+          else st = route_layer(P, I, FS_ROUTE_UNIFORM, sz, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
           if (st != FS_OK) { fail(I, st, l); return; }
           I.routing_calls++;
           log_route(P, I, 0, i + 1, step, l, sz, sm);
@@ -1017,13 +1245,14 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
 }
 
 // ---- the per-instance event loop -------------------------------------------------------------------
-__device__ void simulate_instance(const EngineParams& P, int idx, int lane, WarpSmem* sm) {
+__device__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm) {
   const long long t_start = clock64();
   Inst I;
   const fs_instance_desc* d = &P.descs[idx];
   I.d = d;
   I.idx = idx;
   I.lane = lane;
+  I.slot = slot;
   I.N = d->n_requests;
   I.R = d->n_replicas;
   I.mode = d->mode;
@@ -1118,6 +1347,8 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, Warp
     o.steps_executed = s.steps;
     P.rep_out[I.rb + r] = o;
   }
+  __syncwarp();
+  if (lane == 0 && P.inst_done) atomicAdd(P.inst_done, 1);
 }
 
 __global__ void __launch_bounds__(32 * kWarpsPerCta) sim_kernel(EngineParams P) {
@@ -1129,8 +1360,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) sim_kernel(EngineParams P) 
     if (lane == 0) k = atomicAdd(P.work_counter, 1);
     k = __shfl_sync(FS_FULL, k, 0);
     if (k >= P.n_inst) break;
-    simulate_instance(P, P.order[k], lane, sm);
+    simulate_instance(P, P.order[k], lane, blockIdx.x * kWarpsPerCta + w, sm);
   }
+  if (P.jobs) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w);
 }
 
 __global__ void midstate_kernel(const fs_seed_prefix* pf, uint32_t* mid, int n) {
@@ -1146,14 +1378,23 @@ void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void*
   midstate_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(prefixes, mid, n);
 }
 
-int launch_simulation(const EngineParams& p, int n_sms, void* stream) {
-  if (p.n_inst <= 0) return 0;
+// Persistent grid: every CTA resident at once (the job board relies on warps
+// that run out of instances turning into helpers; correctness does not).
+int simulation_slots(int n_sms, int n_inst) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel, 32 * kWarpsPerCta, 0);
   if (per_sm < 1) per_sm = 1;
-  const int need = (p.n_inst + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int need = (n_inst + kWarpsPerCta - 1) / kWarpsPerCta;
   int grid = n_sms * per_sm;
   if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  return grid * kWarpsPerCta;
+}
+
+int launch_simulation(const EngineParams& p, int n_sms, void* stream) {
+  if (p.n_inst <= 0) return 0;
+  (void)n_sms;
+  const int grid = p.n_slots / kWarpsPerCta;
   sim_kernel<<<grid, 32 * kWarpsPerCta, 0, (cudaStream_t)stream>>>(p);
   return 1;
 }

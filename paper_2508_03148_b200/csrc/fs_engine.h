@@ -32,6 +32,20 @@ struct RepState {
   int32_t pad;
 };
 
+constexpr int kJobLayers = 32;  // layers routed per job
+
+// A routing job: the uniform router calls of up to kJobLayers layers of one
+// batch (routing.py:65-113, one call per layer), split into chunks of rows
+// that any idle warp on the GPU may claim (see fs_engine.cu, "job board").
+struct RouteJob {
+  unsigned long long ctr;  // epoch (24 bits) | n_chunks (20 bits) | next chunk (20 bits)
+  int32_t done;            // chunks finished
+  int32_t tie;             // a boundary tie was seen
+  int64_t T;               // tokens (rows per layer)
+  int32_t E, k, nl, nseg, passes_per_chunk, pad;
+  uint64_t keys[kJobLayers][2];
+};
+
 struct EngineParams {
   // inputs
   const fs_instance_desc* descs;
@@ -67,10 +81,17 @@ struct EngineParams {
   int32_t log_enabled;
   int32_t* work_counter;
   int64_t* inst_cycles;          // SM cycles each instance took (profiling aid)
+  // routing job board (one slot per resident warp of the simulation grid)
+  RouteJob* jobs;
+  int32_t* job_counts;           // [n_slots][kJobLayers * job_max_e]
+  int32_t n_slots;
+  int32_t job_max_e;
+  int32_t* inst_done;            // instances finished (helpers stop at n_inst)
 };
 
 // host-side launchers (fs_engine.cu / fs_metrics.cu / fs_costs.cu)
 void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void* stream);
+int simulation_slots(int n_sms, int n_inst);
 int launch_simulation(const EngineParams& p, int n_sms, void* stream);
 int launch_metrics(const EngineParams& p, void* stream);
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,

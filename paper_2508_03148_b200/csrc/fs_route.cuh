@@ -15,21 +15,46 @@
 
 namespace fs {
 
+// Insert x into the ascending list top[0..kc). Small lists insert branch-free
+// (a compare-exchange chain); larger ones skip the chain when x cannot enter.
 template <int KCAP>
 __device__ __forceinline__ void topk_insert(uint64_t (&top)[KCAP], int kc, uint64_t x,
                                             uint64_t& thr) {
-  if (x >= thr) return;
+  if (KCAP > 4 && x >= thr) return;
 #pragma unroll
   for (int j = 0; j < KCAP; j++) {
     if (j < kc) {
-      uint64_t lo = top[j] < x ? top[j] : x;
+      const uint64_t lo = top[j] < x ? top[j] : x;
       x = top[j] < x ? x : top[j];
       top[j] = lo;
     }
   }
+  if (KCAP > 4) {
 #pragma unroll
-  for (int j = 0; j < KCAP; j++)
-    if (j == kc - 1) thr = top[j];
+    for (int j = 0; j < KCAP; j++)
+      if (j == kc - 1) thr = top[j];
+  }
+}
+
+// Keys of draws [n0, n1) of a fresh Philox stream (numpy pre-increments the
+// counter: draw n is word n % 4 of block n / 4 + 1) inserted into `top`.
+// Each block's four words are consumed by an unrolled, predicated loop so the
+// block stays in registers; `ebase` maps a draw index to its expert index.
+template <int KCAP>
+__device__ __forceinline__ void topk_scan(uint64_t (&top)[KCAP], int kc, uint64_t& thr,
+                                          uint64_t n0, uint64_t n1, uint64_t ebase, uint64_t k0,
+                                          uint64_t k1) {
+  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) {
+    const U4 blk = philox4x64_10(b + 1, k0, k1);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint64_t n = 4 * b + j;
+      if (n >= n0 && n < n1) {
+        const uint64_t packed = ((blk.v[j] >> 11) << 11) | (n - ebase);
+        topk_insert<KCAP>(top, kc, packed, thr);
+      }
+    }
+  }
 }
 
 // Returns FS_OK or FS_ERR_ROUTING_TIE. counts[] (shared, >= E ints) receives the tally.
@@ -64,15 +89,8 @@ __device__ int route_uniform_warp_k(int lane, int64_t T, int E, int k, uint64_t 
     if (active) {
       const int e0 = my_seg * seg_len;
       const int e1 = min(E, e0 + seg_len);
-      uint64_t n = (uint64_t)row * (uint64_t)E + (uint64_t)e0;
-      U4 blk;
-      if (e0 < e1) blk = philox4x64_10(n / 4 + 1, k0, k1);
-      for (int e = e0; e < e1; e++, n++) {
-        const int w = (int)(n & 3);
-        if (w == 0 && e != e0) blk = philox4x64_10(n / 4 + 1, k0, k1);
-        const uint64_t packed = ((blk.v[w] >> 11) << 11) | (uint64_t)e;
-        topk_insert<KCAP>(top, kc, packed, thr);
-      }
+      const uint64_t rb = (uint64_t)row * (uint64_t)E;
+      if (e0 < e1) topk_scan<KCAP>(top, kc, thr, rb + e0, rb + e1, rb, k0, k1);
     }
     // merge the nseg partial lists of each row (all lanes participate in shuffles)
     for (int s = 1; s < nseg; s <<= 1) {
