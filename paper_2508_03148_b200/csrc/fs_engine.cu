@@ -513,27 +513,43 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
     for (int l = 0; l < L; l++) ls.add(tot);  // never L * tot: Python adds layer by layer
   } else {
     const bool board = use_job_board(I.d, d->routing_policy, n);
+    const bool log_routes = P.log_enabled && P.log.routes;
     for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
       const int lend = min(L, l0 + kLayerChunk);
+      double lane_ffn = 0.0, lane_ratio = 1.0;
       if (board) {
-        const int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n);
+        int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n);
+        if (st == FS_OK)
+          st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, n, d->num_experts,
+                                d->top_k, d->d_model, d->expert_d_ff, d->ffn_matrices,
+                                d->dtype_bytes, c.ep, c.moe_tp, d->intra_latency_s,
+                                d->intra_bandwidth_bps, c, &lane_ffn,
+                                moe_out ? &lane_ratio : nullptr);
         if (st != FS_OK) { fail(I, st, l0); return 0.0; }
       } else {
         derive_layer_keys(P, I, rd.prefix, 0, step, l0, L, sm);
       }
       for (int l = l0; l < lend; l++) {
-        int st = FS_OK;
-        if (board) load_job_layer(P, I, l - l0, sm);
-        else st = route_layer(P, I, d->routing_policy, n, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
-        if (st != FS_OK) { fail(I, st, l); return 0.0; }
-        I.routing_calls++;
-        log_route(P, I, r, 0, step, l, n, sm);
         double ffn, ratio = 1.0;
-        st = moe_layer_warp(I.lane, sm->counts, n, d->num_experts, d->top_k, d->d_model,
-                            d->expert_d_ff, d->ffn_matrices, d->dtype_bytes, c.ep, c.moe_tp,
-                            d->intra_latency_s, d->intra_bandwidth_bps, c, &ffn,
-                            moe_out ? &ratio : nullptr);
-        if (st != FS_OK) { fail(I, st, l); return 0.0; }
+        if (board) {
+          ffn = __shfl_sync(FS_FULL, lane_ffn, l - l0);
+          ratio = __shfl_sync(FS_FULL, lane_ratio, l - l0);
+          I.routing_calls++;
+          if (log_routes) {
+            load_job_layer(P, I, l - l0, sm);
+            log_route(P, I, r, 0, step, l, n, sm);
+          }
+        } else {
+          int st = route_layer(P, I, d->routing_policy, n, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
+          if (st != FS_OK) { fail(I, st, l); return 0.0; }
+          I.routing_calls++;
+          log_route(P, I, r, 0, step, l, n, sm);
+          st = moe_layer_warp(I.lane, sm->counts, n, d->num_experts, d->top_k, d->d_model,
+                              d->expert_d_ff, d->ffn_matrices, d->dtype_bytes, c.ep, c.moe_tp,
+                              d->intra_latency_s, d->intra_bandwidth_bps, c, &ffn,
+                              moe_out ? &ratio : nullptr);
+          if (st != FS_OK) { fail(I, st, l); return 0.0; }
+        }
         __syncwarp();
         if (moe_out && I.lane == 0) moe_out[l] = ratio;
         double tot = qkv + att;
@@ -1150,15 +1166,28 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
       for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
         const int lend = min(L, l0 + kLayerChunk);
         if (board) {
-          const int st = run_route_job(P, I, rd.prefix_mb, i + 1, step, l0, lend - l0, sz);
+          int st = run_route_job(P, I, rd.prefix_mb, i + 1, step, l0, lend - l0, sz);
+          double lane_f = 0.0;
+          if (st == FS_OK)
+            st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, sz, d->num_experts,
+                                  d->top_k, d->d_model, d->expert_d_ff, d->ffn_matrices,
+                                  d->dtype_bytes, cf.ep, cf.moe_tp, d->intra_latency_s,
+                                  d->intra_bandwidth_bps, cf, &lane_f, nullptr);
           if (st != FS_OK) { fail(I, st, l0); return; }
-        } else {
-          derive_layer_keys(P, I, rd.prefix_mb, i + 1, step, l0, L, sm);
+          if (I.lane < lend - l0) ffn[(int64_t)i * L + l0 + I.lane] = py_round(lane_f * 1000.0);
+          I.routing_calls += lend - l0;
+          if (P.log_enabled && P.log.routes) {
+            for (int l = l0; l < lend; l++) {
+              load_job_layer(P, I, l - l0, sm);
+              log_route(P, I, 0, i + 1, step, l, sz, sm);
+            }
+          }
+          __syncwarp();
+          continue;
         }
+        derive_layer_keys(P, I, rd.prefix_mb, i + 1, step, l0, L, sm);
         for (int l = l0; l < lend; l++) {
-          int st = FS_OK;
-          if (board) load_job_layer(P, I, l - l0, sm);
-          else st = route_layer(P, I, FS_ROUTE_UNIFORM, sz, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
+          int st = route_layer(P, I, FS_ROUTE_UNIFORM, sz, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
           if (st != FS_OK) { fail(I, st, l); return; }
           I.routing_calls++;
           log_route(P, I, 0, i + 1, step, l, sz, sm);
@@ -1351,7 +1380,10 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
   if (lane == 0 && P.inst_done) atomicAdd(P.inst_done, 1);
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta) sim_kernel(EngineParams P) {
+#ifndef FS_SIM_MIN_BLOCKS
+#define FS_SIM_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerCta, FS_SIM_MIN_BLOCKS) sim_kernel(EngineParams P) {
   __shared__ WarpSmem smem[kWarpsPerCta];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem* sm = &smem[w];

@@ -184,4 +184,50 @@ __device__ inline int moe_layer_warp(int lane, const int* counts, int64_t T, int
   return FS_OK;
 }
 
+// moe_layer_latency for nl layers at once, one layer per lane: lane j < nl reads
+// layer j's tally counts[j*E ...] (global, through L2) and returns that layer's
+// total in *total (and expert / mean(per_rank) in *ratio when non-null). The
+// status is uniform across lanes.
+__device__ inline int moe_layers_lanes(int lane, const int32_t* counts, int nl, int64_t T, int E,
+                                       int top_k, int d_model, int expert_d_ff, int nm, int dt,
+                                       int ep, int moe_tp, double lat, double bw,
+                                       const fs_cost_ctx& c, double* total, double* ratio) {
+  if (ep < 1 || moe_tp < 1 || E % ep != 0 || expert_d_ff % moe_tp != 0)
+    return FS_ERR_TOPOLOGY_MISMATCH;
+  if (T < 1) return FS_ERR_EMPTY_BATCH;
+  const double gate = linear_us(T, E, d_model, c, dt);
+  const int64_t routed_bytes = T * (int64_t)top_k * d_model * dt;
+  const double dispatch = collective_flt(false, i2d(routed_bytes) / (double)ep, ep, lat, bw) * 1e6;
+  const int per = E / ep;
+  const int64_t dffs = expert_d_ff / moe_tp;
+  *total = 0.0;
+  if (ratio) *ratio = 1.0;
+  if (lane < nl) {
+    const int32_t* cl = counts + (int64_t)lane * E;
+    double expert = 0.0;
+    PySum ps;
+    ps.init();
+    for (int r = 0; r < ep; r++) {
+      int64_t routed = 0, active = 0;
+      for (int j = 0; j < per; j++) {
+        const int cnt = __ldcg(cl + r * per + j);
+        routed += cnt;
+        active += cnt > 0;
+      }
+      const double v = routed ? grouped_gemm_us(routed, active, d_model, dffs, nm, c, dt) : 0.0;
+      if (r == 0 || v > expert) expert = v;  // max(): first maximum
+      if (ratio) ps.add(v);
+    }
+    double t = gate + dispatch;
+    t = t + expert;
+    t = t + dispatch;
+    *total = t;
+    if (ratio) {
+      const double s = ps.result();
+      *ratio = s > 0 ? expert / (s / (double)ep) : 1.0;
+    }
+  }
+  return FS_OK;
+}
+
 }  // namespace fs

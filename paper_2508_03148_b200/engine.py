@@ -17,7 +17,7 @@ from . import abi
 from .lower import Lowered
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libfrontier_b200.so")
+LIB_PATH = os.environ.get("FS_ENGINE_LIB", os.path.join(LIB_DIR, "libfrontier_b200.so"))
 
 
 class EngineUnavailable(RuntimeError):
