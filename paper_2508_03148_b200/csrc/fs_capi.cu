@@ -245,8 +245,9 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   for (int i = 0; i < n_instances; i++)
     if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);
   P.job_max_e = std::min(max_e, FS_MAX_EXPERTS);
-  FS_CHECK(e->inst_done.ensure(sizeof(int32_t)));
+  FS_CHECK(e->inst_done.ensure(2 * sizeof(int32_t)));
   P.inst_done = e->inst_done.as<int32_t>();
+  P.open_jobs = e->inst_done.as<int32_t>() + 1;
   if (max_e > 0) {
     FS_CHECK(e->jobs.ensure((size_t)P.n_slots * sizeof(fs::RouteJob)));
     FS_CHECK(e->job_counts.ensure((size_t)P.n_slots * fs::kJobLayers * P.job_max_e * 4));
@@ -271,7 +272,7 @@ int fs_launch_async(fs_engine* e, void* stream) {
   if (!e || !e->staged) return 1;
   cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
   FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
-  FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, sizeof(int32_t), s));
+  FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
   if (e->params.jobs)
     FS_CHECK(cudaMemsetAsync(e->jobs.p, 0, (size_t)e->params.n_slots * sizeof(fs::RouteJob), s));
   e->last_launches = 0;

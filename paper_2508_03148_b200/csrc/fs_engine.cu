@@ -45,6 +45,7 @@ enum { PH_PREFILL = 0, PH_DECODE = 1, PH_AF = 2 };
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kLayerChunk = 32;
+constexpr int kSlabBytes = 12 * 1024;  // per-warp shared-memory slab for hot instance state
 constexpr int32_t kNoFinish = 0x7fffffff;
 
 struct __align__(16) WarpSmem {
@@ -63,6 +64,8 @@ struct Inst {
   int rb;          // global index of local replica 0
   int32_t* lists;  // 3*N ints per replica: queue, running, inflight members
   HEv* heap;
+  RepState* rs;    // replica states (shared-memory slab or HBM)
+  int32_t* fin;    // per-request finish step, local index (slab or HBM)
   int hn;
   int64_t now, seq, events, max_events;
   int rr, n_done, cursor;
@@ -88,12 +91,12 @@ __device__ __forceinline__ void fail(Inst& I, int st, int detail) {
 // ---- replica state: every lane loads the same struct; lane 0 stores -------------
 __device__ __forceinline__ RepState load_rep(const EngineParams& P, const Inst& I, int r) {
   __syncwarp();
-  return P.rstate[I.rb + r];
+  return I.rs[r];
 }
 __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, int r,
                                           const RepState& s) {
   __syncwarp();
-  if (I.lane == 0) P.rstate[I.rb + r] = s;
+  if (I.lane == 0) I.rs[r] = s;
   __syncwarp();
 }
 
@@ -292,14 +295,20 @@ __device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
   return *reinterpret_cast<const volatile int32_t*>(p);
 }
 
-// returns a claimed chunk index or -1 (same on all lanes)
-__device__ int claim_chunk(RouteJob* job, int lane) {
+// returns a claimed chunk index or -1 (same on all lanes). A successful claim is
+// followed by a fence so the job parameters, written before the job was
+// published, are visible; the claimant of the last chunk closes the job.
+__device__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
   long long c = -1;
   if (lane == 0) {
     const unsigned long long v = ld_volatile_u64(&job->ctr);
     if ((v & kChunkMask) < ((v >> kChunkBits) & kChunkMask)) {
       const unsigned long long old = atomicAdd(&job->ctr, 1ull);
-      if ((old & kChunkMask) < ((old >> kChunkBits) & kChunkMask)) c = (long long)(old & kChunkMask);
+      const unsigned long long n = (old >> kChunkBits) & kChunkMask;
+      if ((old & kChunkMask) < n) {
+        c = (long long)(old & kChunkMask);
+        if ((unsigned long long)c + 1 == n) atomicSub(P.open_jobs, 1);
+      }
     }
   }
   c = __shfl_sync(FS_FULL, c, 0);
@@ -307,62 +316,147 @@ __device__ int claim_chunk(RouteJob* job, int lane) {
   return (int)c;
 }
 
+// One pass: lane (row r of `layer`, segment seg) keeps the kc smallest keys of
+// its draws. Fast path: 32-bit surrogate keys (the top 32 bits of each draw,
+// whose order agrees with the 53-bit key except on a tie of those bits) with
+// the expert index in the low `eb` bits; the set is exact unless the k-th and
+// (k+1)-th surrogates tie above the index bits, in which case the pass is
+// redone with the exact 64-bit keys (which also detects a true tie).
 template <int KCAP>
-__device__ void process_chunk_k(RouteJob* job, int32_t* counts, int c, int lane) {
+__device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool active, uint64_t rb,
+                                          int e0, int e1, uint32_t emask, uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) top[j] = 0xFFFFFFFFu;
+  uint32_t thr = 0xFFFFFFFFu;
+  if (!active || e0 >= e1) return;
+  const uint64_t n0 = rb + e0, n1 = rb + e1;
+  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) {
+    const U4 blk = philox4x64_10(b + 1, k0, k1);
+    const uint64_t base = 4 * b;
+    const int jlo = n0 > base ? (int)(n0 - base) : 0;
+    const int jhi = (n1 - base) < 4 ? (int)(n1 - base) : 4;
+    const uint32_t eb0 = (uint32_t)(base - rb);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j >= jlo && j < jhi) {
+        uint32_t x = ((uint32_t)(blk.v[j] >> 32) & ~emask) | (eb0 + (uint32_t)j);
+        if (KCAP <= 4 || x < thr) {
+#pragma unroll
+          for (int q = 0; q < KCAP; q++) {
+            const uint32_t lo = min(top[q], x);
+            x = max(top[q], x);
+            top[q] = lo;
+          }
+          if (KCAP > 4) {
+#pragma unroll
+            for (int q = 0; q < KCAP; q++)
+              if (q == kc - 1) thr = top[q];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int KCAP>
+__device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+                                int lane) {
   const int64_t T = __ldcg(&job->T);
   const int E = __ldcg(&job->E), k = __ldcg(&job->k), nl = __ldcg(&job->nl);
   const int nseg = __ldcg(&job->nseg), ppc = __ldcg(&job->passes_per_chunk);
-  const int rows_per_pass = 32 / nseg;
+  const int rpp = 32 / nseg;
   const int seg_len = (E + nseg - 1) / nseg;
   const int64_t total_rows = (int64_t)nl * T;
   const int kc = k + 1;
-  const int seg = lane % nseg;
+  const int seg = lane & (nseg - 1);
+  const int e0 = seg * seg_len, e1 = min(E, e0 + seg_len);
+  int eb = 0;
+  while ((1 << eb) < E) eb++;
+  const uint32_t emask = (1u << eb) - 1u;
   int tie = 0;
+  // this lane's first row; later passes advance it incrementally (no division)
+  const int64_t row0 = (int64_t)c * ppc * rpp;
+  int64_t row_j = row0 + lane / nseg;
+  int layer = (int)(row_j / T);
+  int64_t r = row_j - (int64_t)layer * T;
+  int key_layer = -1;
+  uint64_t k0 = 0, k1 = 0;
   for (int p = 0; p < ppc; p++) {
-    const int64_t pass_row0 = ((int64_t)c * ppc + p) * rows_per_pass;
-    if (pass_row0 >= total_rows) break;
-    const int64_t row_j = pass_row0 + lane / nseg;
+    if (row0 + (int64_t)p * rpp >= total_rows) break;
     const bool active = row_j < total_rows;
-    uint64_t top[KCAP];
-#pragma unroll
-    for (int j = 0; j < KCAP; j++) top[j] = ~0ull;
-    uint64_t thr = ~0ull;
-    int layer = 0;
-    if (active) {
-      layer = (int)(row_j / T);
-      const int64_t r = row_j - (int64_t)layer * T;
-      const uint64_t k0 = __ldcg(&job->keys[layer][0]), k1 = __ldcg(&job->keys[layer][1]);
-      const int e0 = seg * seg_len, e1 = min(E, e0 + seg_len);
-      const uint64_t rb = (uint64_t)r * (uint64_t)E;
-      if (e0 < e1) topk_scan<KCAP>(top, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+    if (active && layer != key_layer) {
+      k0 = __ldcg(&job->keys[layer][0]);
+      k1 = __ldcg(&job->keys[layer][1]);
+      key_layer = layer;
     }
+    const uint64_t rb = (uint64_t)r * (uint64_t)E;
+    uint32_t top[KCAP];
+    pass_fast<KCAP>(top, kc, active, rb, e0, e1, emask, k0, k1);
     for (int s = 1; s < nseg; s <<= 1) {
-      uint64_t other[KCAP];
+      uint32_t other[KCAP];
 #pragma unroll
       for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, top[j], s);
 #pragma unroll
-      for (int j = 0; j < KCAP; j++)
-        if (j < kc) topk_insert<KCAP>(top, kc, other[j], thr);
+      for (int j = 0; j < KCAP; j++) {
+        uint32_t x = other[j];
+#pragma unroll
+        for (int q = 0; q < KCAP; q++) {
+          const uint32_t lo = min(top[q], x);
+          x = max(top[q], x);
+          top[q] = lo;
+        }
+      }
     }
     const bool leader = active && seg == 0;
+    bool unsure = false;
+#pragma unroll
+    for (int j = 1; j < KCAP; j++)
+      if (j == k && leader && (top[j] >> eb) == (top[j - 1] >> eb)) unsure = true;
+    int ids[KCAP];
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) ids[j] = (int)(top[j] & emask);
+    if (__any_sync(FS_FULL, unsure)) {
+      // exact 64-bit redo of this pass
+      uint64_t t64[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
+      uint64_t thr = ~0ull;
+      if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+      for (int s = 1; s < nseg; s <<= 1) {
+        uint64_t other[KCAP];
+#pragma unroll
+        for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
+#pragma unroll
+        for (int j = 0; j < KCAP; j++)
+          if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
+      }
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) {
+        ids[j] = (int)(t64[j] & 0x7FF);
+        if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < KCAP; j++) {
       if (j < k) {
-        const int key = leader ? layer * E + (int)(top[j] & 0x7FF) : -1;
+        const int key = leader ? layer * E + ids[j] : -1;
         const unsigned grp = __match_any_sync(FS_FULL, key);
         if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counts[key], __popc(grp));
       }
-      if (j == k && leader && ((top[j] >> 11) == (top[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
     }
+    r += rpp;
+    row_j += rpp;
+    while (r >= T) { r -= T; layer++; }
   }
   if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
 }
 
-__device__ void process_chunk(RouteJob* job, int32_t* counts, int c, int lane) {
+__device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+                              int lane) {
   const int k = __ldcg(&job->k);
-  if (k + 1 <= 4) process_chunk_k<4>(job, counts, c, lane);
-  else if (k + 1 <= 9) process_chunk_k<9>(job, counts, c, lane);
-  else process_chunk_k<FS_MAX_TOPK + 1>(job, counts, c, lane);
+  if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane);
+  else if (k + 1 <= 9) process_chunk_k<9>(P, job, counts, c, lane);
+  else process_chunk_k<FS_MAX_TOPK + 1>(P, job, counts, c, lane);
   __threadfence();
   if (lane == 0) atomicAdd(&job->done, 1);
   __syncwarp();
@@ -397,12 +491,15 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
     job->keys[I.lane][1] = key[1];
   }
   for (int i = I.lane; i < nl * E; i += 32) counts[i] = 0;
-  // geometry: split rows into segments while there are few of them
+  // geometry: split rows into segments while there are few of them; a chunk
+  // carries >= ~16 Philox blocks per lane so claims and fences stay cheap
   const int64_t rows = (int64_t)nl * T;
   int nseg = 1;
   while (nseg < 32 && (nseg * 2) * 4 <= E && rows * nseg < 2048) nseg *= 2;
-  const int64_t passes = (rows + (32 / nseg) - 1) / (32 / nseg);
-  int ppc = (int)((passes + 1023) / 1024);
+  const int rpp = 32 / nseg;
+  const int64_t passes = (rows + rpp - 1) / rpp;
+  const int blocks_per_pass = ((E + nseg - 1) / nseg + 3) / 4 + 1;
+  int ppc = 16 / blocks_per_pass;
   if (ppc < 1) ppc = 1;
   int64_t n_chunks = (passes + ppc - 1) / ppc;
   if (n_chunks > kMaxChunks) {
@@ -415,7 +512,7 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
   }
   __syncwarp();
   __threadfence();
-  const bool shared = n_chunks > 2;  // tiny jobs are not worth publishing
+  const bool shared = n_chunks >= 4;  // small jobs are not worth publishing
   if (I.lane == 0) {
     const unsigned long long epoch =
         ((ld_volatile_u64(&job->ctr) >> (2 * kChunkBits)) + 1) & 0xFFFFFFull;
@@ -423,13 +520,14 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
                                  ((unsigned long long)n_chunks << kChunkBits);
     // a private job is published fully claimed, so helpers never see it
     atomicExch(&job->ctr, shared ? v : (v | (unsigned long long)n_chunks));
+    if (shared) atomicAdd(P.open_jobs, 1);
   }
   __syncwarp();
   if (shared) {
-    for (int c; (c = claim_chunk(job, I.lane)) >= 0;) process_chunk(job, counts, c, I.lane);
+    for (int c; (c = claim_chunk(P, job, I.lane)) >= 0;) process_chunk(P, job, counts, c, I.lane);
     while (ld_volatile_i32(&job->done) < n_chunks) __nanosleep(64);
   } else {
-    for (int c = 0; c < n_chunks; c++) process_chunk(job, counts, c, I.lane);
+    for (int c = 0; c < n_chunks; c++) process_chunk(P, job, counts, c, I.lane);
   }
   __threadfence();
   __syncwarp();
@@ -453,14 +551,21 @@ __device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, Warp
 }
 
 // warps with no instance left help route other warps' jobs until every
-// instance has finished
+// instance has finished; they sleep (exponential backoff) while no job is open
 __device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
   const int ns = P.n_slots;
-  const unsigned rot = (unsigned)my_slot * 2654435761u;
+  const int start = (int)(((unsigned)my_slot * 37u) % (unsigned)ns);
+  unsigned backoff = 32;
   while (ld_volatile_i32(P.inst_done) < P.n_inst) {
-    bool found = false;
+    if (ld_volatile_i32(P.open_jobs) <= 0) {
+      __nanosleep(backoff);
+      backoff = backoff < 4096 ? backoff * 2 : 4096;
+      continue;
+    }
+    backoff = 32;
     for (int base = 0; base < ns; base += 32) {
-      const int s = (int)((rot + (unsigned)(base + lane)) % (unsigned)ns);
+      int s = start + base + lane;
+      if (s >= ns) s -= ns;
       bool avail = false;
       if (base + lane < ns) {
         const unsigned long long v = ld_volatile_u64(&P.jobs[s].ctr);
@@ -472,13 +577,10 @@ __device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
         m &= m - 1;
         const int sp = __shfl_sync(FS_FULL, s, pick);
         RouteJob* job = &P.jobs[sp];
-        for (int c; (c = claim_chunk(job, lane)) >= 0;) {
-          process_chunk(job, job_counts_of(P, sp), c, lane);
-          found = true;
-        }
+        for (int c; (c = claim_chunk(P, job, lane)) >= 0;)
+          process_chunk(P, job, job_counts_of(P, sp), c, lane);
       }
     }
-    if (!found) __nanosleep(256);
   }
 }
 
@@ -840,7 +942,7 @@ __device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& 
     const int out = P.output[gi(I, req)];
     const int32_t f = s.dstep + (out - emitted);
     rl[s.rlen + __popc(hm & lt)] = req;
-    P.finish_at[gi(I, req)] = f;
+    I.fin[req] = f;
     ctx = (int64_t)P.prompt[gi(I, req)] + emitted;
     fin = f;
   }
@@ -906,7 +1008,7 @@ __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& 
     const int i = base + I.lane;
     const bool valid = i < s.rlen;
     const int req = valid ? rl[i] : 0;
-    const int32_t f = valid ? P.finish_at[gi(I, req)] : kNoFinish;
+    const int32_t f = valid ? I.fin[req] : kNoFinish;
     const bool fin = valid && f == s.dstep;
     const unsigned fm = __ballot_sync(FS_FULL, fin);
     const unsigned km = __ballot_sync(FS_FULL, valid && !fin);
@@ -991,7 +1093,7 @@ __device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_u
   for (int r = I.lane; r < I.R; r += 32) {
     const fs_replica_desc& rd = P.reps[I.rb + r];
     if (rd.role != role) continue;
-    const RepState& st = P.rstate[I.rb + r];
+    const RepState& st = I.rs[r];
     const int64_t v = by_used ? st.used : st.outstanding;
     if (v < best_v || (v == best_v && rd.key_rank < best_rank)) {
       best_v = v; best_rank = rd.key_rank; best_r = r;
@@ -1140,7 +1242,7 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
     int64_t ctx = 0;
     for (int j = I.lane; j < w; j += 32) {
       const int req = rl[off + j];
-      ctx += (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)] + s.dstep - P.finish_at[gi(I, req)];
+      ctx += (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)] + s.dstep - I.fin[req];
     }
     ctx = warp_sum_i64(ctx);
     double us = qkv_us(d, ca, w) + attn_cost_us(d, ca, attention_decode_flops(ctx, hd), w, ctx);
@@ -1274,7 +1376,19 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
 }
 
 // ---- the per-instance event loop -------------------------------------------------------------------
-__device__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm) {
+// Bytes of per-instance hot state (replica states, event heap, queue / running /
+// inflight lists, finish steps); kept in the warp's shared-memory slab when it
+// fits, in HBM otherwise (generic pointers make both paths the same code).
+__device__ __forceinline__ int64_t slab_need(int R, int N) {
+  const int64_t rs = (int64_t)R * sizeof(RepState);
+  const int64_t heap = ((int64_t)R + N + 8) * sizeof(HEv);
+  const int64_t lists = 3LL * R * (N > 0 ? N : 1) * 4;
+  const int64_t fin = ((int64_t)N * 4 + 15) / 16 * 16;
+  return rs + heap + lists + fin;
+}
+
+__device__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm,
+                                  char* slab) {
   const long long t_start = clock64();
   Inst I;
   const fs_instance_desc* d = &P.descs[idx];
@@ -1287,8 +1401,21 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
   I.mode = d->mode;
   I.ro = d->req_offset;
   I.rb = d->replica_offset;
-  I.lists = P.lists + P.list_base[idx];
-  I.heap = P.heap + P.heap_base[idx];
+  if (slab && slab_need(I.R, I.N) <= kSlabBytes) {
+    char* p = slab;
+    I.rs = reinterpret_cast<RepState*>(p);
+    p += (int64_t)I.R * sizeof(RepState);
+    I.heap = reinterpret_cast<HEv*>(p);
+    p += ((int64_t)I.R + I.N + 8) * sizeof(HEv);
+    I.fin = reinterpret_cast<int32_t*>(p);
+    p += ((int64_t)I.N * 4 + 15) / 16 * 16;
+    I.lists = reinterpret_cast<int32_t*>(p);
+  } else {
+    I.rs = P.rstate + I.rb;
+    I.heap = P.heap + P.heap_base[idx];
+    I.fin = P.finish_at + I.ro;
+    I.lists = P.lists + P.list_base[idx];
+  }
   I.hn = 0;
   I.now = 0;
   I.seq = 0;
@@ -1311,7 +1438,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
     s.used = 0; s.outstanding = 0; s.steps = 0; s.busy_ns = 0; s.sum_ctx = 0; s.inflight_dur = 0;
     s.qlen = 0; s.rlen = 0; s.ilen = 0; s.busy = 0; s.start_pending = 0; s.dstep = 0;
     s.min_finish = kNoFinish; s.inflight_phase = 0; s.inflight_moe = 0; s.pad = 0;
-    P.rstate[I.rb + r] = s;
+    I.rs[r] = s;
   }
   __syncwarp();
 
@@ -1369,7 +1496,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
     if (P.inst_cycles) P.inst_cycles[idx] = clock64() - t_start;
   }
   for (int r = lane; r < I.R; r += 32) {
-    const RepState s = P.rstate[I.rb + r];
+    const RepState s = I.rs[r];
     fs_replica_out o;
     o.busy_ns = s.busy_ns;
     o.busy_fraction = 0.0;
@@ -1385,14 +1512,16 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
 #endif
 __global__ void __launch_bounds__(32 * kWarpsPerCta, FS_SIM_MIN_BLOCKS) sim_kernel(EngineParams P) {
   __shared__ WarpSmem smem[kWarpsPerCta];
+  extern __shared__ __align__(16) char slabs[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem* sm = &smem[w];
+  char* slab = slabs + (int64_t)w * kSlabBytes;
   for (;;) {
     int k = 0;
     if (lane == 0) k = atomicAdd(P.work_counter, 1);
     k = __shfl_sync(FS_FULL, k, 0);
     if (k >= P.n_inst) break;
-    simulate_instance(P, P.order[k], lane, blockIdx.x * kWarpsPerCta + w, sm);
+    simulate_instance(P, P.order[k], lane, blockIdx.x * kWarpsPerCta + w, sm, slab);
   }
   if (P.jobs) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w);
 }
@@ -1412,9 +1541,20 @@ void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void*
 
 // Persistent grid: every CTA resident at once (the job board relies on warps
 // that run out of instances turning into helpers; correctness does not).
+static size_t sim_dyn_smem() {
+  static bool configured = false;
+  const size_t bytes = (size_t)kWarpsPerCta * kSlabBytes;
+  if (!configured) {
+    cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    configured = true;
+  }
+  return bytes;
+}
+
 int simulation_slots(int n_sms, int n_inst) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel, 32 * kWarpsPerCta, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel, 32 * kWarpsPerCta,
+                                                sim_dyn_smem());
   if (per_sm < 1) per_sm = 1;
   const int need = (n_inst + kWarpsPerCta - 1) / kWarpsPerCta;
   int grid = n_sms * per_sm;
@@ -1427,7 +1567,7 @@ int launch_simulation(const EngineParams& p, int n_sms, void* stream) {
   if (p.n_inst <= 0) return 0;
   (void)n_sms;
   const int grid = p.n_slots / kWarpsPerCta;
-  sim_kernel<<<grid, 32 * kWarpsPerCta, 0, (cudaStream_t)stream>>>(p);
+  sim_kernel<<<grid, 32 * kWarpsPerCta, sim_dyn_smem(), (cudaStream_t)stream>>>(p);
   return 1;
 }
 

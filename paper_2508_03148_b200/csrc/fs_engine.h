@@ -87,6 +87,7 @@ struct EngineParams {
   int32_t n_slots;
   int32_t job_max_e;
   int32_t* inst_done;            // instances finished (helpers stop at n_inst)
+  int32_t* open_jobs;            // published jobs with unclaimed chunks
 };
 
 // host-side launchers (fs_engine.cu / fs_metrics.cu / fs_costs.cu)
