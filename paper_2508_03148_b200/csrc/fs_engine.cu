@@ -34,6 +34,8 @@
 // scalar writes are issued by lane 0 and ordered with __syncwarp().
 #include <cuda_runtime.h>
 
+// cost helpers out of line here: instruction-cache footprint of the DES kernel
+#define FS_COST_INLINE __noinline__
 #include "fs_device.cuh"
 #include "fs_engine.h"
 #include "fs_route.cuh"
@@ -104,7 +106,7 @@ __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, 
 __device__ __forceinline__ bool hev_less(const HEv& a, const HEv& b) {
   return a.t < b.t || (a.t == b.t && a.seq < b.seq);
 }
-__device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
+__device__ __noinline__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   if (t < I.now) { fail(I, FS_ERR_SCHEDULING_IN_PAST, kind); return; }
   __syncwarp();
   if (I.lane == 0) {
@@ -124,7 +126,7 @@ __device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   I.seq++;
   __syncwarp();
 }
-__device__ HEv heap_pop(Inst& I) {
+__device__ __noinline__ HEv heap_pop(Inst& I) {
   HEv top;
   top.t = 0; top.seq = 0; top.kind = 0; top.a = 0; top.b = 0;
   __syncwarp();
@@ -198,7 +200,7 @@ __device__ __forceinline__ double attn_cost_us(const fs_instance_desc* d, const 
 }
 
 // ---- router seeds for 32 layers at a time, one layer per lane --------------------------
-__device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int prefix, int mb,
+__device__ __noinline__ void derive_layer_keys(const EngineParams& P, const Inst& I, int prefix, int mb,
                                   int64_t step, int l0, int L, WarpSmem* sm) {
   __syncwarp();
   const int layer = l0 + I.lane;
@@ -220,7 +222,7 @@ __device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int pref
 }
 
 // ---- one router call (routing.py:65-113) ------------------------------------------------
-__device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
+__device__ __noinline__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
                            uint64_t k0, uint64_t k1, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   const int E = d->num_experts, k = d->top_k;
@@ -244,15 +246,18 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
     if (neg || s != T * k) return FS_ERR_ROUTING;
     return FS_OK;
   }
-  if (T == 0 || k == E || policy == FS_ROUTE_UNIFORM) {
-    if (T > 0 && k < E && k > FS_MAX_TOPK) return FS_ERR_CAPACITY;
+  if (T == 0 || k == E) {  // RNG-free shortcuts (routing.py:90-94)
     __syncwarp();
-    return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
+    for (int e = I.lane; e < E; e += 32) sm->counts[e] = T == 0 ? 0 : (int)T;
+    __syncwarp();
+    return FS_OK;
   }
+  // every other uniform call runs on the job board (use_job_board)
+  if (policy == FS_ROUTE_UNIFORM) return FS_ERR_CAPACITY;
   return FS_ERR_UNSUPPORTED;  // dirichlet_skew is not on the device path yet
 }
 
-__device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
+__device__ __noinline__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
                           int64_t T, const WarpSmem* sm) {
   if (!P.log_enabled || !P.log.routes) return;
   const int E = I.d->num_experts;
@@ -298,7 +303,7 @@ __device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
 // returns a claimed chunk index or -1 (same on all lanes). A successful claim is
 // followed by a fence so the job parameters, written before the job was
 // published, are visible; the claimant of the last chunk closes the job.
-__device__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
+__device__ __noinline__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
   long long c = -1;
   if (lane == 0) {
     const unsigned long long v = ld_volatile_u64(&job->ctr);
@@ -330,11 +335,19 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
   uint32_t thr = 0xFFFFFFFFu;
   if (!active || e0 >= e1) return;
   const uint64_t n0 = rb + e0, n1 = rb + e1;
-  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) {
-    const U4 blk = philox4x64_10(b + 1, k0, k1);
+  const uint64_t blast = (n1 - 1) >> 2;
+  // two blocks per iteration: independent multiply chains interleave (ILP)
+  for (uint64_t b2 = n0 >> 2; b2 <= blast; b2 += 2) {
+    U4 pair[2];
+    pair[0] = philox4x64_10(b2 + 1, k0, k1);
+    pair[1] = philox4x64_10(b2 + 2, k0, k1);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+    const uint64_t b = b2 + h;
+    const U4& blk = pair[h];
     const uint64_t base = 4 * b;
     const int jlo = n0 > base ? (int)(n0 - base) : 0;
-    const int jhi = (n1 - base) < 4 ? (int)(n1 - base) : 4;
+    const int jhi = b > blast ? 0 : ((n1 - base) < 4 ? (int)(n1 - base) : 4);
     const uint32_t eb0 = (uint32_t)(base - rb);
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -355,11 +368,12 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
         }
       }
     }
+    }
   }
 }
 
 template <int KCAP>
-__device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+__device__ __noinline__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
                                 int lane) {
   const int64_t T = __ldcg(&job->T);
   const int E = __ldcg(&job->E), k = __ldcg(&job->k), nl = __ldcg(&job->nl);
@@ -451,7 +465,7 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
   if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
 }
 
-__device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+__device__ __noinline__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
                               int lane) {
   const int k = __ldcg(&job->k);
   if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane);
@@ -468,7 +482,7 @@ __device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slo
 
 // Route layers [l0, l0+nl) of one batch; the tally of layer l0+j ends up at
 // job_counts_of(slot)[j*E ...]. Returns FS_OK or FS_ERR_ROUTING_TIE.
-__device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
+__device__ __noinline__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
                              int l0, int nl, int64_t T) {
   const fs_instance_desc* d = I.d;
   RouteJob* job = &P.jobs[I.slot];
@@ -542,7 +556,7 @@ __device__ __forceinline__ bool use_job_board(const fs_instance_desc* d, int pol
 }
 
 // copy one layer's tally from the job (through L2) to the warp's counts
-__device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, WarpSmem* sm) {
+__device__ __noinline__ void load_job_layer(const EngineParams& P, const Inst& I, int j, WarpSmem* sm) {
   const int E = I.d->num_experts;
   const int32_t* counts = job_counts_of(P, I.slot) + (int64_t)j * E;
   __syncwarp();
@@ -552,7 +566,7 @@ __device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, Warp
 
 // warps with no instance left help route other warps' jobs until every
 // instance has finished; they sleep (exponential backoff) while no job is open
-__device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
+__device__ __noinline__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
   const int ns = P.n_slots;
   const int start = (int)(((unsigned)my_slot * 37u) % (unsigned)ns);
   unsigned backoff = 32;
@@ -592,7 +606,7 @@ struct BatchShape {
 
 // Duration in us (same on all lanes). moe_out (global) receives per-layer raw
 // moe_imbalance ratios when non-null.
-__device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
+__device__ __noinline__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
                                 const BatchShape& b, int64_t step, WarpSmem* sm,
                                 double* moe_out) {
   const fs_instance_desc* d = I.d;
@@ -680,7 +694,7 @@ __device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
   I.log_eoff += I.d->num_layers;
   return off + 1;
 }
-__device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
+__device__ __noinline__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
                           const int32_t* members, int nm, int32_t moe_off1) {
   if (!P.log_enabled || !P.log.batches) return;
   const int n_moe = moe_off1 ? I.d->num_layers : 0;
@@ -707,7 +721,7 @@ __device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int6
 
 // ---- list helpers ---------------------------------------------------------------------------
 // remove the first m entries (stable shift)
-__device__ void list_drop_front(int32_t* a, int len, int m, int lane) {
+__device__ __noinline__ void list_drop_front(int32_t* a, int len, int m, int lane) {
   if (m == 0) return;
   for (int base = 0; base < len - m; base += 32) {
     const int i = base + lane;
@@ -718,7 +732,7 @@ __device__ void list_drop_front(int32_t* a, int len, int m, int lane) {
   }
 }
 // insert v at position pos (shifting the tail right)
-__device__ void list_insert(int32_t* a, int len, int pos, int v, int lane) {
+__device__ __noinline__ void list_insert(int32_t* a, int len, int pos, int v, int lane) {
   for (int top = len; top > pos; top -= 32) {
     const int i = top - 1 - lane;  // source index, descending
     const bool act = i >= pos;
@@ -743,7 +757,7 @@ __device__ __forceinline__ bool prio_less(const EngineParams& P, const Inst& I, 
 }
 
 // enqueue a waiting request; priority admission keeps the queue in key order
-__device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
+__device__ __noinline__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
   int32_t* q = qlist(I, r);
   if (I.d->admission == FS_ADMIT_PRIORITY) {
     int pos = 0;
@@ -763,7 +777,7 @@ __device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int 
 
 // FIFO head of a queue (the queue in priority mode is key-ordered; the FIFO
 // head is the earliest-arrived request, i.e. the smallest local index)
-__device__ int queue_head(const Inst& I, int r, const RepState& s) {
+__device__ __noinline__ int queue_head(const Inst& I, int r, const RepState& s) {
   const int32_t* q = qlist(I, r);
   if (I.d->admission != FS_ADMIT_PRIORITY) return q[0];
   int64_t m = 0x7fffffff;
@@ -778,7 +792,7 @@ struct Admit {
 };
 
 // Admitted members (candidate order) go to the inflight list and leave the queue.
-__device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
+__device__ __noinline__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
                                int running_count, int64_t capacity) {
   const fs_instance_desc* d = I.d;
   int32_t* q = qlist(I, r);
@@ -863,7 +877,7 @@ __device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& 
 }
 
 // ---- batch launch helpers ----------------------------------------------------------------------
-__device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ __noinline__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, const BatchShape& b, int phase,
                              WarpSmem* sm) {
   const int32_t moe_off1 = log_moe_reserve(P, I);
@@ -879,7 +893,7 @@ __device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
 }
 
-__device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ __noinline__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
                               const fs_replica_desc& rd, const Admit& A, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -911,7 +925,7 @@ __device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s
   launch_batch(P, I, r, s, rd, b, PH_PREFILL, sm);
 }
 
-__device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ __noinline__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -924,7 +938,7 @@ __device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
   launch_batch(P, I, r, s, rd, b, PH_DECODE, sm);
 }
 
-__device__ void kick(Inst& I, int r, RepState& s) {
+__device__ __noinline__ void kick(Inst& I, int r, RepState& s) {
   if (s.busy || s.start_pending) return;
   if (s.qlen == 0 && s.rlen == 0) return;
   s.start_pending = 1;
@@ -932,7 +946,7 @@ __device__ void kick(Inst& I, int r, RepState& s) {
 }
 
 // append requests (cooperatively: lane i holds req if has) to the running list
-__device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
+__device__ __noinline__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
                                int req, int emitted) {
   const unsigned lt = (1u << I.lane) - 1u;
   const unsigned hm = __ballot_sync(FS_FULL, has);
@@ -954,7 +968,7 @@ __device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& 
 
 // prefill completion (colocated.py:70-91, pd.py:98-112, af.py:514-535).
 // to_running: co-located / AF; otherwise PD (unfinished go to the transfer FIFO).
-__device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ __noinline__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
                                  bool to_running) {
   const fs_instance_desc* d = I.d;
   const int32_t* il = ilist(I, r);
@@ -994,7 +1008,7 @@ __device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState
 // decode / AF completion: every member emitted one token; finished requests leave
 // the running list in order (colocated.py:92-107, pd.py:113-127, af.py:536-551).
 // Returns the number finished. pool charge per finished request = rounded(prompt+output).
-__device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
+__device__ __noinline__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // TOKEN_EMITTED
   s.dstep++;
@@ -1037,7 +1051,7 @@ __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& 
 }
 
 // ---- co-located (colocated.py) ------------------------------------------------------------------
-__device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
+__device__ __noinline__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   const int r = I.rr % I.R;
   I.rr++;
   RepState s = load_rep(P, I, r);
@@ -1046,10 +1060,10 @@ __device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   store_rep(P, I, r, s);
 }
 
-__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+__device__ __noinline__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm);
 
-__device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+__device__ __noinline__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
   if (!s.busy) {
@@ -1068,7 +1082,7 @@ __device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* 
   store_rep(P, I, r, s);
 }
 
-__device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+__device__ __noinline__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1087,7 +1101,7 @@ __device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t
 
 // ---- PD (pd.py) ---------------------------------------------------------------------------------
 // argmin over replicas of `role` by (key value, key_rank); value from rstate
-__device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
+__device__ __noinline__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
   int64_t best_v = INT64_MAX;
   int best_rank = 0x7fffffff, best_r = -1;
   for (int r = I.lane; r < I.R; r += 32) {
@@ -1109,7 +1123,7 @@ __device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_u
   return best_r;
 }
 
-__device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
+__device__ __noinline__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
   __syncwarp();
   const int r = pd_pick(P, I, FS_ROLE_PREFILL, false);
   RepState s = load_rep(P, I, r);
@@ -1121,7 +1135,7 @@ __device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
 }
 
 // _pump_transfers (pd.py:141-192): strict FIFO, decode replica by (used, key)
-__device__ void pd_pump(const EngineParams& P, Inst& I) {
+__device__ __noinline__ void pd_pump(const EngineParams& P, Inst& I) {
   const fs_instance_desc* d = I.d;
   while (I.xt > I.xh && I.status == FS_OK) {
     const int req = P.xfer[I.ro + I.xh % I.N];
@@ -1142,7 +1156,7 @@ __device__ void pd_pump(const EngineParams& P, Inst& I) {
   }
 }
 
-__device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+__device__ __noinline__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
@@ -1174,7 +1188,7 @@ __device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* 
   store_rep(P, I, r, s);
 }
 
-__device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+__device__ __noinline__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1196,7 +1210,7 @@ __device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t
   store_rep(P, I, r, s);
 }
 
-__device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
+__device__ __noinline__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // MEMORY_AVAILABLE
   __syncwarp();
@@ -1218,7 +1232,7 @@ __device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req
 }
 
 // ---- AF step (af.py:244-319, 468-507) ------------------------------------------------------------
-__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+__device__ __noinline__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   const int L = d->num_layers;
@@ -1387,7 +1401,7 @@ __device__ __forceinline__ int64_t slab_need(int R, int N) {
   return rs + heap + lists + fin;
 }
 
-__device__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm,
+__device__ __noinline__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm,
                                   char* slab) {
   const long long t_start = clock64();
   Inst I;

@@ -114,3 +114,27 @@ def test_attention_cost_bulk_vs_oracle(engine):
     for b in range(0, 4096, 97):
         s, e = off[b], off[b + 1]
         assert out[b] == oracle.attention_us(bool(dec[b]), q[s:e], kv[s:e], 32, 8, 128, 2.25e15, 8e12)
+
+
+def test_sweep_driver_end_to_end(engine, tmp_path):
+    """run_sweep on the GPU: ok rows equal the oracle's metrics, failures become rows."""
+    import csv
+
+    from oracle import oracle
+    from paper_2508_03148_b200.sweep import grid_points, point_documents, run_sweep
+    doc = W.c1_colocated(24, seed=11)
+    cfg = parse_config(copy.deepcopy(doc))
+    grid = {"policies.max_num_seqs": [4, 32], "clusters.0.hardware.hbm_capacity_bytes": [11.2e9, 180e9]}
+    summary = run_sweep(cfg, grid, str(tmp_path), engine=engine)
+    assert summary["points"] == 4
+    with open(tmp_path / "sweep.csv") as fh:
+        rows = list(csv.DictReader(fh))
+    docs = point_documents(cfg.to_document(), grid_points(grid), cfg.seed)
+    low = lower([instance_spec(parse_config(d)) for d in docs])
+    ref = oracle.run(low)
+    for r, st, thr in zip(rows, ref.rows["status"], ref.rows["throughput_tokens_per_s_per_gpu"]):
+        if st == 0:
+            assert r["status"] == "ok" and float(r["throughput_tokens_per_s_per_gpu"]) == thr
+        else:
+            assert r["status"].startswith("failed: RequestCannotFit")
+    assert (tmp_path / "frontier.json").exists()
