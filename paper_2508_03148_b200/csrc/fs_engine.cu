@@ -34,8 +34,6 @@
 // scalar writes are issued by lane 0 and ordered with __syncwarp().
 #include <cuda_runtime.h>
 
-// cost helpers out of line here: instruction-cache footprint of the DES kernel
-#define FS_COST_INLINE __noinline__
 #include "fs_device.cuh"
 #include "fs_engine.h"
 #include "fs_route.cuh"
@@ -106,7 +104,7 @@ __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, 
 __device__ __forceinline__ bool hev_less(const HEv& a, const HEv& b) {
   return a.t < b.t || (a.t == b.t && a.seq < b.seq);
 }
-__device__ __noinline__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
+__device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   if (t < I.now) { fail(I, FS_ERR_SCHEDULING_IN_PAST, kind); return; }
   __syncwarp();
   if (I.lane == 0) {
@@ -126,7 +124,7 @@ __device__ __noinline__ void heap_push(Inst& I, int64_t t, int kind, int a, int6
   I.seq++;
   __syncwarp();
 }
-__device__ __noinline__ HEv heap_pop(Inst& I) {
+__device__ HEv heap_pop(Inst& I) {
   HEv top;
   top.t = 0; top.seq = 0; top.kind = 0; top.a = 0; top.b = 0;
   __syncwarp();
@@ -303,7 +301,7 @@ __device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
 // returns a claimed chunk index or -1 (same on all lanes). A successful claim is
 // followed by a fence so the job parameters, written before the job was
 // published, are visible; the claimant of the last chunk closes the job.
-__device__ __noinline__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
+__device__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
   long long c = -1;
   if (lane == 0) {
     const unsigned long long v = ld_volatile_u64(&job->ctr);
@@ -372,8 +370,36 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
   }
 }
 
+// Exact 64-bit redo of one pass (rare: only when 32-bit surrogates tie at the
+// selection boundary). Writes the chosen experts to ids; returns 1 on a true tie.
 template <int KCAP>
-__device__ __noinline__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+__device__ __noinline__ int exact_pass(int* ids, int k, int nseg, bool active, bool leader,
+                                       uint64_t rb, int e0, int e1, uint64_t k0, uint64_t k1) {
+  const int kc = k + 1;
+  int tie = 0;
+  uint64_t t64[KCAP];
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
+  uint64_t thr = ~0ull;
+  if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+  for (int s = 1; s < nseg; s <<= 1) {
+    uint64_t other[KCAP];
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
+#pragma unroll
+    for (int j = 0; j < KCAP; j++)
+      if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
+  }
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) {
+    ids[j] = (int)(t64[j] & 0x7FF);
+    if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
+  }
+  return tie;
+}
+
+template <int KCAP>
+__device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
                                 int lane) {
   const int64_t T = __ldcg(&job->T);
   const int E = __ldcg(&job->E), k = __ldcg(&job->k), nl = __ldcg(&job->nl);
@@ -429,27 +455,7 @@ __device__ __noinline__ void process_chunk_k(const EngineParams& P, RouteJob* jo
     int ids[KCAP];
 #pragma unroll
     for (int j = 0; j < KCAP; j++) ids[j] = (int)(top[j] & emask);
-    if (__any_sync(FS_FULL, unsure)) {
-      // exact 64-bit redo of this pass
-      uint64_t t64[KCAP];
-#pragma unroll
-      for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
-      uint64_t thr = ~0ull;
-      if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
-      for (int s = 1; s < nseg; s <<= 1) {
-        uint64_t other[KCAP];
-#pragma unroll
-        for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
-#pragma unroll
-        for (int j = 0; j < KCAP; j++)
-          if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
-      }
-#pragma unroll
-      for (int j = 0; j < KCAP; j++) {
-        ids[j] = (int)(t64[j] & 0x7FF);
-        if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
-      }
-    }
+    if (__any_sync(FS_FULL, unsure)) tie |= exact_pass<KCAP>(ids, k, nseg, active, leader, rb, e0, e1, k0, k1);
 #pragma unroll
     for (int j = 0; j < KCAP; j++) {
       if (j < k) {
@@ -465,7 +471,7 @@ __device__ __noinline__ void process_chunk_k(const EngineParams& P, RouteJob* jo
   if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
 }
 
-__device__ __noinline__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+__device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
                               int lane) {
   const int k = __ldcg(&job->k);
   if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane);
@@ -482,7 +488,7 @@ __device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slo
 
 // Route layers [l0, l0+nl) of one batch; the tally of layer l0+j ends up at
 // job_counts_of(slot)[j*E ...]. Returns FS_OK or FS_ERR_ROUTING_TIE.
-__device__ __noinline__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
+__device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
                              int l0, int nl, int64_t T) {
   const fs_instance_desc* d = I.d;
   RouteJob* job = &P.jobs[I.slot];
@@ -606,7 +612,7 @@ struct BatchShape {
 
 // Duration in us (same on all lanes). moe_out (global) receives per-layer raw
 // moe_imbalance ratios when non-null.
-__device__ __noinline__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
+__device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
                                 const BatchShape& b, int64_t step, WarpSmem* sm,
                                 double* moe_out) {
   const fs_instance_desc* d = I.d;
@@ -721,7 +727,7 @@ __device__ __noinline__ void log_batch(const EngineParams& P, Inst& I, int r, in
 
 // ---- list helpers ---------------------------------------------------------------------------
 // remove the first m entries (stable shift)
-__device__ __noinline__ void list_drop_front(int32_t* a, int len, int m, int lane) {
+__device__ void list_drop_front(int32_t* a, int len, int m, int lane) {
   if (m == 0) return;
   for (int base = 0; base < len - m; base += 32) {
     const int i = base + lane;
@@ -757,7 +763,7 @@ __device__ __forceinline__ bool prio_less(const EngineParams& P, const Inst& I, 
 }
 
 // enqueue a waiting request; priority admission keeps the queue in key order
-__device__ __noinline__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
+__device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
   int32_t* q = qlist(I, r);
   if (I.d->admission == FS_ADMIT_PRIORITY) {
     int pos = 0;
@@ -792,7 +798,7 @@ struct Admit {
 };
 
 // Admitted members (candidate order) go to the inflight list and leave the queue.
-__device__ __noinline__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
+__device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
                                int running_count, int64_t capacity) {
   const fs_instance_desc* d = I.d;
   int32_t* q = qlist(I, r);
@@ -877,7 +883,7 @@ __device__ __noinline__ Admit admit_prefill(const EngineParams& P, Inst& I, int 
 }
 
 // ---- batch launch helpers ----------------------------------------------------------------------
-__device__ __noinline__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, const BatchShape& b, int phase,
                              WarpSmem* sm) {
   const int32_t moe_off1 = log_moe_reserve(P, I);
@@ -893,7 +899,7 @@ __device__ __noinline__ void launch_batch(const EngineParams& P, Inst& I, int r,
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
 }
 
-__device__ __noinline__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
                               const fs_replica_desc& rd, const Admit& A, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -925,7 +931,7 @@ __device__ __noinline__ void start_prefill(const EngineParams& P, Inst& I, int r
   launch_batch(P, I, r, s, rd, b, PH_PREFILL, sm);
 }
 
-__device__ __noinline__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -938,7 +944,7 @@ __device__ __noinline__ void start_decode(const EngineParams& P, Inst& I, int r,
   launch_batch(P, I, r, s, rd, b, PH_DECODE, sm);
 }
 
-__device__ __noinline__ void kick(Inst& I, int r, RepState& s) {
+__device__ void kick(Inst& I, int r, RepState& s) {
   if (s.busy || s.start_pending) return;
   if (s.qlen == 0 && s.rlen == 0) return;
   s.start_pending = 1;
@@ -946,7 +952,7 @@ __device__ __noinline__ void kick(Inst& I, int r, RepState& s) {
 }
 
 // append requests (cooperatively: lane i holds req if has) to the running list
-__device__ __noinline__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
+__device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
                                int req, int emitted) {
   const unsigned lt = (1u << I.lane) - 1u;
   const unsigned hm = __ballot_sync(FS_FULL, has);
@@ -968,7 +974,7 @@ __device__ __noinline__ void running_append(const EngineParams& P, Inst& I, int 
 
 // prefill completion (colocated.py:70-91, pd.py:98-112, af.py:514-535).
 // to_running: co-located / AF; otherwise PD (unfinished go to the transfer FIFO).
-__device__ __noinline__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
                                  bool to_running) {
   const fs_instance_desc* d = I.d;
   const int32_t* il = ilist(I, r);
@@ -1008,7 +1014,7 @@ __device__ __noinline__ void prefill_complete(const EngineParams& P, Inst& I, in
 // decode / AF completion: every member emitted one token; finished requests leave
 // the running list in order (colocated.py:92-107, pd.py:113-127, af.py:536-551).
 // Returns the number finished. pool charge per finished request = rounded(prompt+output).
-__device__ __noinline__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
+__device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // TOKEN_EMITTED
   s.dstep++;
@@ -1051,7 +1057,7 @@ __device__ __noinline__ int decode_complete(const EngineParams& P, Inst& I, int 
 }
 
 // ---- co-located (colocated.py) ------------------------------------------------------------------
-__device__ __noinline__ void co_arrival(const EngineParams& P, Inst& I, int req) {
+__device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   const int r = I.rr % I.R;
   I.rr++;
   RepState s = load_rep(P, I, r);
@@ -1063,7 +1069,7 @@ __device__ __noinline__ void co_arrival(const EngineParams& P, Inst& I, int req)
 __device__ __noinline__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm);
 
-__device__ __noinline__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+__device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
   if (!s.busy) {
@@ -1082,7 +1088,7 @@ __device__ __noinline__ void co_batch_start(const EngineParams& P, Inst& I, int 
   store_rep(P, I, r, s);
 }
 
-__device__ __noinline__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+__device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1101,7 +1107,7 @@ __device__ __noinline__ void co_batch_complete(const EngineParams& P, Inst& I, i
 
 // ---- PD (pd.py) ---------------------------------------------------------------------------------
 // argmin over replicas of `role` by (key value, key_rank); value from rstate
-__device__ __noinline__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
+__device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
   int64_t best_v = INT64_MAX;
   int best_rank = 0x7fffffff, best_r = -1;
   for (int r = I.lane; r < I.R; r += 32) {
@@ -1123,7 +1129,7 @@ __device__ __noinline__ int pd_pick(const EngineParams& P, const Inst& I, int ro
   return best_r;
 }
 
-__device__ __noinline__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
+__device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
   __syncwarp();
   const int r = pd_pick(P, I, FS_ROLE_PREFILL, false);
   RepState s = load_rep(P, I, r);
@@ -1135,7 +1141,7 @@ __device__ __noinline__ void pd_arrival(const EngineParams& P, Inst& I, int req)
 }
 
 // _pump_transfers (pd.py:141-192): strict FIFO, decode replica by (used, key)
-__device__ __noinline__ void pd_pump(const EngineParams& P, Inst& I) {
+__device__ void pd_pump(const EngineParams& P, Inst& I) {
   const fs_instance_desc* d = I.d;
   while (I.xt > I.xh && I.status == FS_OK) {
     const int req = P.xfer[I.ro + I.xh % I.N];
@@ -1156,7 +1162,7 @@ __device__ __noinline__ void pd_pump(const EngineParams& P, Inst& I) {
   }
 }
 
-__device__ __noinline__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+__device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
@@ -1188,7 +1194,7 @@ __device__ __noinline__ void pd_batch_start(const EngineParams& P, Inst& I, int 
   store_rep(P, I, r, s);
 }
 
-__device__ __noinline__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+__device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1210,7 +1216,7 @@ __device__ __noinline__ void pd_batch_complete(const EngineParams& P, Inst& I, i
   store_rep(P, I, r, s);
 }
 
-__device__ __noinline__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
+__device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // MEMORY_AVAILABLE
   __syncwarp();
@@ -1401,7 +1407,7 @@ __device__ __forceinline__ int64_t slab_need(int R, int N) {
   return rs + heap + lists + fin;
 }
 
-__device__ __noinline__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm,
+__device__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm,
                                   char* slab) {
   const long long t_start = clock64();
   Inst I;
