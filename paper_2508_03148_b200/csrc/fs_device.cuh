@@ -10,12 +10,6 @@
 
 #define FS_FULL 0xffffffffu
 
-// Cost-model helpers are called once per iteration in the simulation kernel,
-// whose code size (instruction-cache footprint) matters more than call overhead.
-#ifndef FS_COST_INLINE
-#define FS_COST_INLINE __forceinline__
-#endif
-
 namespace fs {
 
 // ---------------------------------------------------------------------------
@@ -51,13 +45,13 @@ struct PySum {
 // ---------------------------------------------------------------------------
 // Analytic cost model (costmodel/analytic.py:18-71, topology.py:360-394)
 // ---------------------------------------------------------------------------
-static __device__ FS_COST_INLINE double roofline_us(double flops, double nbytes, const fs_cost_ctx& h) {
+__device__ __forceinline__ double roofline_us(double flops, double nbytes, const fs_cost_ctx& h) {
   double sec = py_max(flops / h.peak_flops, nbytes / h.mem_bw);
   return h.kernel_overhead_us + sec * 1e6;
 }
 
 // analytic.py:23-29 linear_us(m, n, k)
-static __device__ FS_COST_INLINE double linear_us(int64_t m, int64_t n, int64_t k, const fs_cost_ctx& h,
+__device__ __forceinline__ double linear_us(int64_t m, int64_t n, int64_t k, const fs_cost_ctx& h,
                                             int dt) {
   double flops = 2.0 * i2d(m);
   flops = flops * i2d(n);
@@ -67,7 +61,7 @@ static __device__ FS_COST_INLINE double linear_us(int64_t m, int64_t n, int64_t 
 }
 
 // topology.py:367-394, integer bytes_per_rank (int*int, then int/int true division)
-static __device__ FS_COST_INLINE double collective_int(bool all_reduce, int64_t bpr, int n, double lat,
+__device__ __forceinline__ double collective_int(bool all_reduce, int64_t bpr, int n, double lat,
                                                  double bw) {
   if (n == 1) return 0.0;
   double wire = i2d(bpr * (int64_t)(n - 1)) / (double)n;
@@ -76,7 +70,7 @@ static __device__ FS_COST_INLINE double collective_int(bool all_reduce, int64_t 
   return lat + wire;
 }
 // float bytes_per_rank (moe.py:81-85)
-static __device__ FS_COST_INLINE double collective_flt(bool all_reduce, double bpr, int n, double lat,
+__device__ __forceinline__ double collective_flt(bool all_reduce, double bpr, int n, double lat,
                                                  double bw) {
   if (n == 1) return 0.0;
   double wire = bpr * (double)(n - 1);
@@ -87,7 +81,7 @@ static __device__ FS_COST_INLINE double collective_flt(bool all_reduce, double b
 }
 
 // analytic.py:56-71 over one rank's (routed, active) summary
-static __device__ FS_COST_INLINE double grouped_gemm_us(int64_t routed, int64_t active, int64_t d_model,
+__device__ __forceinline__ double grouped_gemm_us(int64_t routed, int64_t active, int64_t d_model,
                                                   int64_t d_ff, int nm, const fs_cost_ctx& h,
                                                   int dt) {
   double flops = 2.0 * (double)nm;
@@ -100,7 +94,7 @@ static __device__ FS_COST_INLINE double grouped_gemm_us(int64_t routed, int64_t 
 }
 
 // analytic.py:46-53 given the batch sums; `flops` precomputed by the caller
-static __device__ FS_COST_INLINE double attention_us_from(double flops, int64_t sum_q, int64_t sum_kv,
+__device__ __forceinline__ double attention_us_from(double flops, int64_t sum_q, int64_t sum_kv,
                                                     int hq, int hkv, int hdim,
                                                     const fs_cost_ctx& h, int dt) {
   double kvb = 2.0 * i2d(sum_kv);
@@ -144,7 +138,7 @@ __constant__ uint32_t kSha256K[64] = {
 
 __device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
 
-static __device__ __noinline__ void sha256_compress(uint32_t h[8], const uint32_t wblk[16]) {
+__device__ inline void sha256_compress(uint32_t h[8], const uint32_t wblk[16]) {
   uint32_t w[16];
 #pragma unroll
   for (int i = 0; i < 16; i++) w[i] = wblk[i];
@@ -174,7 +168,7 @@ static __device__ __noinline__ void sha256_compress(uint32_t h[8], const uint32_
 // Message = prefix[mid_blocks*64 .. len) ++ ascii(ints joined by ':'), hashed from
 // the midstate `mid` (state after the first mid_blocks full blocks of the prefix).
 // Returns int.from_bytes(sha256(msg)[:4], "big").
-static __device__ __noinline__ uint32_t sha256_tail_first_word(const uint32_t mid[8], int mid_blocks,
+__device__ inline uint32_t sha256_tail_first_word(const uint32_t mid[8], int mid_blocks,
                                                   const uint8_t* prefix, int plen,
                                                   const int64_t* ints, int nints) {
   uint32_t wbuf[32];  // up to two 64-byte blocks
@@ -271,7 +265,7 @@ __device__ __forceinline__ int int_words(uint64_t v, uint32_t* w) {
 }
 // Philox key of np.random.Philox(SeedSequence([seed, 0xE0]).generate_state(2, u64)):
 // the state array is passed as `seed`, so it goes through a second SeedSequence.
-static __device__ __noinline__ void routing_key(uint64_t seed, uint64_t key[2]) {
+__device__ inline void routing_key(uint64_t seed, uint64_t key[2]) {
   uint32_t ent[8];
   int n = int_words(seed, ent);
   n += int_words(0xE0u, ent + n);

@@ -198,7 +198,7 @@ __device__ __forceinline__ double attn_cost_us(const fs_instance_desc* d, const 
 }
 
 // ---- router seeds for 32 layers at a time, one layer per lane --------------------------
-__device__ __noinline__ void derive_layer_keys(const EngineParams& P, const Inst& I, int prefix, int mb,
+__device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int prefix, int mb,
                                   int64_t step, int l0, int L, WarpSmem* sm) {
   __syncwarp();
   const int layer = l0 + I.lane;
@@ -220,7 +220,7 @@ __device__ __noinline__ void derive_layer_keys(const EngineParams& P, const Inst
 }
 
 // ---- one router call (routing.py:65-113) ------------------------------------------------
-__device__ __noinline__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
+__device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
                            uint64_t k0, uint64_t k1, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   const int E = d->num_experts, k = d->top_k;
@@ -244,18 +244,15 @@ __device__ __noinline__ int route_layer(const EngineParams& P, const Inst& I, in
     if (neg || s != T * k) return FS_ERR_ROUTING;
     return FS_OK;
   }
-  if (T == 0 || k == E) {  // RNG-free shortcuts (routing.py:90-94)
+  if (T == 0 || k == E || policy == FS_ROUTE_UNIFORM) {
+    if (T > 0 && k < E && k > FS_MAX_TOPK) return FS_ERR_CAPACITY;
     __syncwarp();
-    for (int e = I.lane; e < E; e += 32) sm->counts[e] = T == 0 ? 0 : (int)T;
-    __syncwarp();
-    return FS_OK;
+    return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
   }
-  // every other uniform call runs on the job board (use_job_board)
-  if (policy == FS_ROUTE_UNIFORM) return FS_ERR_CAPACITY;
   return FS_ERR_UNSUPPORTED;  // dirichlet_skew is not on the device path yet
 }
 
-__device__ __noinline__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
+__device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
                           int64_t T, const WarpSmem* sm) {
   if (!P.log_enabled || !P.log.routes) return;
   const int E = I.d->num_experts;
@@ -333,19 +330,11 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
   uint32_t thr = 0xFFFFFFFFu;
   if (!active || e0 >= e1) return;
   const uint64_t n0 = rb + e0, n1 = rb + e1;
-  const uint64_t blast = (n1 - 1) >> 2;
-  // two blocks per iteration: independent multiply chains interleave (ILP)
-  for (uint64_t b2 = n0 >> 2; b2 <= blast; b2 += 2) {
-    U4 pair[2];
-    pair[0] = philox4x64_10(b2 + 1, k0, k1);
-    pair[1] = philox4x64_10(b2 + 2, k0, k1);
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-    const uint64_t b = b2 + h;
-    const U4& blk = pair[h];
+  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) {
+    const U4 blk = philox4x64_10(b + 1, k0, k1);
     const uint64_t base = 4 * b;
     const int jlo = n0 > base ? (int)(n0 - base) : 0;
-    const int jhi = b > blast ? 0 : ((n1 - base) < 4 ? (int)(n1 - base) : 4);
+    const int jhi = (n1 - base) < 4 ? (int)(n1 - base) : 4;
     const uint32_t eb0 = (uint32_t)(base - rb);
 #pragma unroll
     for (int j = 0; j < 4; j++) {
@@ -366,36 +355,7 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
         }
       }
     }
-    }
   }
-}
-
-// Exact 64-bit redo of one pass (rare: only when 32-bit surrogates tie at the
-// selection boundary). Writes the chosen experts to ids; returns 1 on a true tie.
-template <int KCAP>
-__device__ __noinline__ int exact_pass(int* ids, int k, int nseg, bool active, bool leader,
-                                       uint64_t rb, int e0, int e1, uint64_t k0, uint64_t k1) {
-  const int kc = k + 1;
-  int tie = 0;
-  uint64_t t64[KCAP];
-#pragma unroll
-  for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
-  uint64_t thr = ~0ull;
-  if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
-  for (int s = 1; s < nseg; s <<= 1) {
-    uint64_t other[KCAP];
-#pragma unroll
-    for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
-#pragma unroll
-    for (int j = 0; j < KCAP; j++)
-      if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
-  }
-#pragma unroll
-  for (int j = 0; j < KCAP; j++) {
-    ids[j] = (int)(t64[j] & 0x7FF);
-    if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
-  }
-  return tie;
 }
 
 template <int KCAP>
@@ -455,7 +415,27 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
     int ids[KCAP];
 #pragma unroll
     for (int j = 0; j < KCAP; j++) ids[j] = (int)(top[j] & emask);
-    if (__any_sync(FS_FULL, unsure)) tie |= exact_pass<KCAP>(ids, k, nseg, active, leader, rb, e0, e1, k0, k1);
+    if (__any_sync(FS_FULL, unsure)) {
+      // exact 64-bit redo of this pass
+      uint64_t t64[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
+      uint64_t thr = ~0ull;
+      if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+      for (int s = 1; s < nseg; s <<= 1) {
+        uint64_t other[KCAP];
+#pragma unroll
+        for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
+#pragma unroll
+        for (int j = 0; j < KCAP; j++)
+          if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
+      }
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) {
+        ids[j] = (int)(t64[j] & 0x7FF);
+        if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < KCAP; j++) {
       if (j < k) {
@@ -562,7 +542,7 @@ __device__ __forceinline__ bool use_job_board(const fs_instance_desc* d, int pol
 }
 
 // copy one layer's tally from the job (through L2) to the warp's counts
-__device__ __noinline__ void load_job_layer(const EngineParams& P, const Inst& I, int j, WarpSmem* sm) {
+__device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, WarpSmem* sm) {
   const int E = I.d->num_experts;
   const int32_t* counts = job_counts_of(P, I.slot) + (int64_t)j * E;
   __syncwarp();
@@ -572,7 +552,7 @@ __device__ __noinline__ void load_job_layer(const EngineParams& P, const Inst& I
 
 // warps with no instance left help route other warps' jobs until every
 // instance has finished; they sleep (exponential backoff) while no job is open
-__device__ __noinline__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
+__device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
   const int ns = P.n_slots;
   const int start = (int)(((unsigned)my_slot * 37u) % (unsigned)ns);
   unsigned backoff = 32;
@@ -700,7 +680,7 @@ __device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
   I.log_eoff += I.d->num_layers;
   return off + 1;
 }
-__device__ __noinline__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
+__device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
                           const int32_t* members, int nm, int32_t moe_off1) {
   if (!P.log_enabled || !P.log.batches) return;
   const int n_moe = moe_off1 ? I.d->num_layers : 0;
@@ -738,7 +718,7 @@ __device__ void list_drop_front(int32_t* a, int len, int m, int lane) {
   }
 }
 // insert v at position pos (shifting the tail right)
-__device__ __noinline__ void list_insert(int32_t* a, int len, int pos, int v, int lane) {
+__device__ void list_insert(int32_t* a, int len, int pos, int v, int lane) {
   for (int top = len; top > pos; top -= 32) {
     const int i = top - 1 - lane;  // source index, descending
     const bool act = i >= pos;
@@ -783,7 +763,7 @@ __device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int 
 
 // FIFO head of a queue (the queue in priority mode is key-ordered; the FIFO
 // head is the earliest-arrived request, i.e. the smallest local index)
-__device__ __noinline__ int queue_head(const Inst& I, int r, const RepState& s) {
+__device__ int queue_head(const Inst& I, int r, const RepState& s) {
   const int32_t* q = qlist(I, r);
   if (I.d->admission != FS_ADMIT_PRIORITY) return q[0];
   int64_t m = 0x7fffffff;
@@ -1066,7 +1046,7 @@ __device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   store_rep(P, I, r, s);
 }
 
-__device__ __noinline__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm);
 
 __device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
@@ -1238,7 +1218,7 @@ __device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req
 }
 
 // ---- AF step (af.py:244-319, 468-507) ------------------------------------------------------------
-__device__ __noinline__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   const int L = d->num_layers;

@@ -127,7 +127,7 @@ __device__ inline int route_uniform_warp(int lane, int64_t T, int E, int k, uint
 // moe_layer_latency from a tally in shared memory. All lanes return the same
 // total; *ratio (if non-null) gets expert / mean(per_rank) (base.py:247-252).
 // Returns FS_OK or a status.
-static __device__ __noinline__ int moe_layer_warp(int lane, const int* counts, int64_t T, int E, int top_k,
+__device__ inline int moe_layer_warp(int lane, const int* counts, int64_t T, int E, int top_k,
                                      int d_model, int expert_d_ff, int nm, int dt, int ep,
                                      int moe_tp, double lat, double bw, const fs_cost_ctx& c,
                                      double* total, double* ratio) {
@@ -188,7 +188,7 @@ static __device__ __noinline__ int moe_layer_warp(int lane, const int* counts, i
 // layer j's tally counts[j*E ...] (global, through L2) and returns that layer's
 // total in *total (and expert / mean(per_rank) in *ratio when non-null). The
 // status is uniform across lanes.
-static __device__ __noinline__ int moe_layers_lanes(int lane, const int32_t* counts, int nl, int64_t T, int E,
+__device__ inline int moe_layers_lanes(int lane, const int32_t* counts, int nl, int64_t T, int E,
                                        int top_k, int d_model, int expert_d_ff, int nm, int dt,
                                        int ep, int moe_tp, double lat, double bw,
                                        const fs_cost_ctx& c, double* total, double* ratio) {
