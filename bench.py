@@ -48,6 +48,7 @@ def parse_args():
     ap.add_argument("--seeds", type=int, default=64, help="trace seeds per config (64 -> 4096)")
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 attention-cost kernel leg")
     ap.add_argument("--cpu-sample-seeds", type=int, default=2)
     return ap.parse_args()
 
@@ -189,6 +190,57 @@ def algorithmic_bytes(low, rows) -> int:
     return 16 * memberships + inputs + outputs + 0 * int(np.int64(0))
 
 
+def bench_attention_cost(eng, device: int, steps: int, warmup: int, n_batches: int = 1 << 20):
+    """C2: analytic refined-attention cost over 2^20 skewed 72-request batches.
+
+    HBM-bound segmented reduction (csrc/fs_costs.cu). Inputs (~0.6 GB) exceed
+    the 126 MB L2, so no flush is needed between steps. Returns a dict for
+    the bench line.
+    """
+    import torch
+
+    from paper_2508_03148_b200 import workloads as W
+    from paper_2508_03148_b200.engine import attn_params
+    q, kv, off, dec = W.attention_batches(n_batches)
+    dev = f"cuda:{device}"
+    tq = torch.from_numpy(q).to(dev)
+    tkv = torch.from_numpy(kv).to(dev)
+    toff = torch.from_numpy(off).to(dev)
+    tdec = torch.from_numpy(dec).to(dev)
+    out = torch.empty(n_batches, dtype=torch.float64, device=dev)
+    st = torch.empty(n_batches, dtype=torch.int32, device=dev)
+    prm = attn_params(32, 8, 128, 2, 2.25e15, 8e12, 5.0)
+    stream = torch.cuda.Stream(device=device)
+
+    def launch():
+        eng.attention_cost_dev(tq.data_ptr(), tkv.data_ptr(), toff.data_ptr(), tdec.data_ptr(),
+                               n_batches, prm, out.data_ptr(), st.data_ptr(), stream.cuda_stream)
+
+    for _ in range(max(warmup, 1)):
+        launch()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for s, e in ev:
+        s.record(stream)
+        launch()
+        e.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(s.elapsed_time(e) for s, e in ev) / steps
+    n_el = int(off[-1])
+    alg = 8 * n_el + 8 * (n_batches + 1) + n_batches + 8 * n_batches + 4 * n_batches
+    peak, kind = measured_peaks()
+    gbs = alg / (ms / 1e3) / 1e9
+    ok = bool((st == 0).all().item())
+    return {"workload": f"{n_batches} batches x 72 requests, lognormal(6.5,1.4) kv lengths, "
+                        "alternating decode / prefill", "batches_per_s": n_batches / (ms / 1e3),
+            "ms_per_launch": ms, "algorithmic_bytes_per_launch": alg,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak, "traffic": ncu_traffic("attention_cost_kernel"),
+                         "peak_source": kind},
+            "all_status_ok": ok}
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
@@ -297,6 +349,10 @@ def main():
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     traffic = ncu_traffic("sim_kernel")
 
+    c2 = None
+    if not args.no_c2:
+        c2 = bench_attention_cost(eng, local, args.steps, args.warmup)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_count()
@@ -328,6 +384,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "gather_ms": gather_ms,
             "step_ms": step_ms,
+            "c2_attention_cost": c2,
         }
         print(json.dumps(line))
     if world > 1:
