@@ -106,16 +106,121 @@ __global__ void attention_cost_kernel(const int32_t* __restrict__ q, const int32
   }
 }
 
+// Same reduction with kU batches in flight per warp: the offsets of kU batches,
+// then every lane's 128-bit loads of all kU batches are issued before any
+// reduction, so a warp keeps 2*kU independent 16-byte loads outstanding.
+// Batches that are unaligned or longer than 128 requests take the generic loop.
+constexpr int kU = 4;
+
+__device__ __forceinline__ void acc_from_int4(AttnAcc& a, int4 qv, int4 kvv, int n, bool dec,
+                                              double hd) {
+  if (n > 0) attn_acc(a, qv.x, kvv.x, dec, hd);
+  if (n > 1) attn_acc(a, qv.y, kvv.y, dec, hd);
+  if (n > 2) attn_acc(a, qv.z, kvv.z, dec, hd);
+  if (n > 3) attn_acc(a, qv.w, kvv.w, dec, hd);
+}
+
+__global__ void __launch_bounds__(256) attention_cost_kernel_u(
+    const int32_t* __restrict__ q, const int32_t* __restrict__ kv,
+    const int64_t* __restrict__ off, const uint8_t* __restrict__ dec, int64_t nb,
+    fs_attn_params prm, double* __restrict__ out, int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t hd = (int64_t)prm.num_query_heads * prm.head_dim;
+  const double hdd = (double)hd;
+  fs_cost_ctx h;
+  h.peak_flops = prm.peak_flops; h.mem_bw = prm.mem_bw; h.kernel_overhead_us = prm.kernel_overhead_us;
+  h.tp = h.ep = h.moe_tp = h.pp = 1;
+  for (int64_t g = warp * kU; g < nb; g += nwarps * kU) {
+    int64_t o0[kU], o1[kU];
+    bool dv[kU], fast[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const int64_t b = g + u;
+      const bool valid = b < nb;
+      o0[u] = valid ? __ldg(off + b) : 0;
+      o1[u] = valid ? __ldg(off + b + 1) : 0;
+      dv[u] = valid ? __ldg(dec + b) != 0 : false;
+      fast[u] = (o0[u] & 3) == 0 && o1[u] - o0[u] <= 128;
+    }
+    int4 qv[kU], kvv[kU];
+    int nh[kU];
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const int64_t i = o0[u] + 4 * lane;
+      nh[u] = 0;
+      qv[u] = make_int4(0, 0, 0, 0);
+      kvv[u] = make_int4(0, 0, 0, 0);
+      if (fast[u] && i < o1[u]) {
+        nh[u] = (int)min((int64_t)4, o1[u] - i);
+        if (nh[u] == 4) {
+          qv[u] = __ldg(reinterpret_cast<const int4*>(q + i));
+          kvv[u] = __ldg(reinterpret_cast<const int4*>(kv + i));
+        } else {
+          qv[u].x = __ldg(q + i); kvv[u].x = __ldg(kv + i);
+          if (nh[u] > 1) { qv[u].y = __ldg(q + i + 1); kvv[u].y = __ldg(kv + i + 1); }
+          if (nh[u] > 2) { qv[u].z = __ldg(q + i + 2); kvv[u].z = __ldg(kv + i + 2); }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const int64_t b = g + u;
+      if (b >= nb) break;  // uniform across the warp
+      AttnAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0};
+      if (fast[u]) {
+        acc_from_int4(a, qv[u], kvv[u], nh[u], dv[u], hdd);
+      } else {
+        for (int64_t i = o0[u] + lane; i < o1[u]; i += 32)
+          attn_acc(a, __ldg(q + i), __ldg(kv + i), dv[u], hdd);
+      }
+      const int64_t sq = warp_sum_i64(a.sq), skv = warp_sum_i64(a.skv);
+      const int bad = __any_sync(FS_FULL, a.bad_q | a.bad_kv | (dv[u] ? a.bad_dec : a.bad_pre));
+      int st = FS_OK;
+      if (o1[u] <= o0[u]) st = FS_ERR_EMPTY_BATCH;
+      else if (bad) st = FS_ERR_VALUE;
+      double flops;
+      if (dv[u]) {
+        flops = attention_decode_flops(skv, hd);
+      } else {
+        const int64_t s_eq = warp_sum_i64(a.s_eq), s_ne = warp_sum_i64(a.s_ne);
+        double mt = a.max_term;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mt = fmax(mt, __shfl_xor_sync(FS_FULL, mt, o));
+        const double total_est = 4.0 * hdd * (double)s_ne + 2.0 * hdd * (double)s_eq;
+        if (mt < kTwo53 * 0.5 && total_est < kTwo53 * 0.5) {
+          flops = i2d(4 * hd * s_ne + 2 * hd * s_eq);  // exact integer sum == sequential fp64 sum
+        } else {
+          double tot = 0.0;  // sequential, member order (analytic.py:37-43)
+          if (lane == 0)
+            for (int64_t i = o0[u]; i < o1[u]; i++) tot = tot + attention_prefill_term(q[i], kv[i], hd);
+          flops = __shfl_sync(FS_FULL, tot, 0);
+        }
+      }
+      if (lane == u) {
+        const double us = attention_us_from(flops, sq, skv, prm.num_query_heads,
+                                            prm.num_kv_heads, prm.head_dim, h, prm.dtype_bytes);
+        out[b] = st == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
+        if (status) status[b] = st;
+      }
+    }
+  }
+}
+
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,
                           const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out,
                           int32_t* status, int n_sms, void* stream) {
   if (nb <= 0) return 0;
   const int threads = 256;
-  int64_t blocks = (nb * 32 + threads - 1) / threads;
-  const int64_t cap = (int64_t)n_sms * 8;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attention_cost_kernel_u, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = (nb + (threads / 32) * kU - 1) / ((threads / 32) * kU);
+  const int64_t cap = (int64_t)n_sms * per_sm;  // one resident wave, grid-stride beyond
   if (blocks > cap) blocks = cap;
-  attention_cost_kernel<<<(int)blocks, threads, 0, (cudaStream_t)stream>>>(q, kv, off, dec, nb, prm,
-                                                                          out, status);
+  attention_cost_kernel_u<<<(int)blocks, threads, 0, (cudaStream_t)stream>>>(q, kv, off, dec, nb,
+                                                                            prm, out, status);
   return 1;
 }
 

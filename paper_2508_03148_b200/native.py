@@ -1,20 +1,27 @@
-"""Build of the CUDA engine library (nvcc, sm_100a) into paper_2508_03148_b200/lib/."""
+"""Build of the CUDA engine library (nvcc, sm_100a) into paper_2508_03148_b200/lib/.
+
+Each translation unit is compiled to its own object (in parallel, and only when
+it or a header changed), then linked into libfrontier_b200.so. Device code
+never calls across translation units, so no relocatable device code is needed.
+"""
 
 from __future__ import annotations
 
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libfrontier_b200.so")
+OBJ = os.path.join(HERE, "lib", "obj")
 SOURCES = ["fs_engine.cu", "fs_metrics.cu", "fs_costs.cu", "fs_capi.cu"]
 HEADERS = ["fs_device.cuh", "fs_route.cuh", "fs_engine.h"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
+    *ARCH, "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",  # no FMA contraction: fp64 must follow Python's operation order
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -25,23 +32,49 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def _headers() -> list[str]:
+    hs = [os.path.join(CSRC, h) for h in HEADERS]
+    hs.append(os.path.join(os.path.dirname(HERE), "include", "frontier_b200.h"))
+    return hs
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps.append(os.path.join(os.path.dirname(HERE), "include", "frontier_b200.h"))
+    t = os.path.getmtime(target)
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *[os.path.join(CSRC, f) for f in SOURCES]]
+def stale() -> bool:
+    deps = [os.path.join(CSRC, f) for f in SOURCES] + _headers()
+    return _stale(LIB, deps)
+
+
+def _compile(src: str, verbose: bool, extra: list[str]) -> str:
+    out = _obj(src)
+    if not _stale(out, [os.path.join(CSRC, src)] + _headers()) and not extra:
+        return out
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", out + ".tmp", os.path.join(CSRC, src)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
+
+
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          out: str | None = None) -> str:
+    target = out or LIB
+    if not force and not extra and not stale() and os.path.exists(target):
+        return target
+    os.makedirs(OBJ, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose, extra or []), SOURCES))
+    tmp = target + ".tmp"
+    subprocess.run([nvcc(), *ARCH, "-shared", "-o", tmp, *objs], check=True)
+    os.replace(tmp, target)
+    return target
