@@ -37,87 +37,38 @@ __device__ __forceinline__ void attn_acc(AttnAcc& a, int64_t l, int64_t c, bool 
   a.max_term = a.max_term > t ? a.max_term : t;
 }
 
-__global__ void attention_cost_kernel(const int32_t* __restrict__ q, const int32_t* __restrict__ kv,
-                                      const int64_t* __restrict__ off,
-                                      const uint8_t* __restrict__ dec, int64_t nb,
-                                      fs_attn_params prm, double* __restrict__ out,
-                                      int32_t* __restrict__ status) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t hd = (int64_t)prm.num_query_heads * prm.head_dim;
-  const double hdd = (double)hd;
-  fs_cost_ctx h;
-  h.peak_flops = prm.peak_flops; h.mem_bw = prm.mem_bw; h.kernel_overhead_us = prm.kernel_overhead_us;
-  h.tp = h.ep = h.moe_tp = h.pp = 1;
-  for (int64_t b = warp; b < nb; b += nwarps) {
-    const int64_t o0 = __ldg(off + b), o1 = __ldg(off + b + 1);
-    const bool is_dec = __ldg(dec + b) != 0;
-    AttnAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0};
-    if ((o0 & 3) == 0) {
-      // 128-bit path: lane j covers elements o0 + 4*j .. +3 of each 128-element window
-      for (int64_t base = o0; base < o1; base += 128) {
-        const int64_t i = base + 4 * lane;
-        if (i + 3 < o1) {
-          const int4 qv = __ldg(reinterpret_cast<const int4*>(q + i));
-          const int4 kvv = __ldg(reinterpret_cast<const int4*>(kv + i));
-          attn_acc(a, qv.x, kvv.x, is_dec, hdd);
-          attn_acc(a, qv.y, kvv.y, is_dec, hdd);
-          attn_acc(a, qv.z, kvv.z, is_dec, hdd);
-          attn_acc(a, qv.w, kvv.w, is_dec, hdd);
-        } else {
-          for (int64_t j = i; j < o1 && j < i + 4; j++) attn_acc(a, __ldg(q + j), __ldg(kv + j), is_dec, hdd);
-        }
-      }
-    } else {
-      for (int64_t i = o0 + lane; i < o1; i += 32) attn_acc(a, __ldg(q + i), __ldg(kv + i), is_dec, hdd);
-    }
-    const int64_t sq = warp_sum_i64(a.sq), skv = warp_sum_i64(a.skv);
-    const int64_t s_eq = warp_sum_i64(a.s_eq), s_ne = warp_sum_i64(a.s_ne);
-    const int bad_q = __any_sync(FS_FULL, a.bad_q), bad_dec = __any_sync(FS_FULL, a.bad_dec);
-    const int bad_pre = __any_sync(FS_FULL, a.bad_pre), bad_kv = __any_sync(FS_FULL, a.bad_kv);
-    double mt = a.max_term;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mt = fmax(mt, __shfl_xor_sync(FS_FULL, mt, o));
-    // AttentionFeatures.__post_init__ checks (features.py:79-95)
-    int st = FS_OK;
-    if (o1 <= o0) st = FS_ERR_EMPTY_BATCH;
-    else if (bad_q || (is_dec && bad_dec) || (!is_dec && bad_pre) || bad_kv) st = FS_ERR_VALUE;
-    double flops;
-    if (is_dec) {
-      flops = attention_decode_flops(skv, hd);
-    } else {
-      const double total_est = 4.0 * hdd * (double)s_ne + 2.0 * hdd * (double)s_eq;
-      if (mt < kTwo53 * 0.5 && total_est < kTwo53 * 0.5) {
-        flops = i2d(4 * hd * s_ne + 2 * hd * s_eq);  // exact integer sum == sequential fp64 sum
-      } else {
-        double tot = 0.0;  // sequential, member order (analytic.py:37-43)
-        if (lane == 0)
-          for (int64_t i = o0; i < o1; i++) tot = tot + attention_prefill_term(q[i], kv[i], hd);
-        flops = __shfl_sync(FS_FULL, tot, 0);
-      }
-    }
-    const double us = attention_us_from(flops, sq, skv, prm.num_query_heads, prm.num_kv_heads,
-                                        prm.head_dim, h, prm.dtype_bytes);
-    if (lane == 0) {
-      out[b] = st == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
-      if (status) status[b] = st;
-    }
-  }
-}
-
-// Same reduction with kU batches in flight per warp: the offsets of kU batches,
-// then every lane's 128-bit loads of all kU batches are issued before any
-// reduction, so a warp keeps 2*kU independent 16-byte loads outstanding.
-// Batches that are unaligned or longer than 128 requests take the generic loop.
+// kU batches in flight per warp: the offsets of kU batches, then every lane's
+// 128-bit loads of all kU batches are issued before any reduction, so a warp
+// keeps 2*kU independent 16-byte loads outstanding. Decode batches reduce only
+// sum(kv) (q == 1 is validated by ballot); prefill batches reduce sum(q),
+// sum(kv) and the c == l / c != l products. Lane u then finishes batch u's
+// roofline, so the fp64 tail runs once for all kU batches. Batches that are
+// unaligned or longer than 128 requests take a generic strided loop.
 constexpr int kU = 4;
 
-__device__ __forceinline__ void acc_from_int4(AttnAcc& a, int4 qv, int4 kvv, int n, bool dec,
-                                              double hd) {
-  if (n > 0) attn_acc(a, qv.x, kvv.x, dec, hd);
-  if (n > 1) attn_acc(a, qv.y, kvv.y, dec, hd);
-  if (n > 2) attn_acc(a, qv.z, kvv.z, dec, hd);
-  if (n > 3) attn_acc(a, qv.w, kvv.w, dec, hd);
+struct Lanes4 {
+  int4 q, kv;
+  int n;
+};
+
+__device__ __forceinline__ void acc4(int64_t& sq, int64_t& skv, int64_t& seq, int64_t& sne,
+                                     int64_t& mlc, int& bad, const Lanes4& x, bool dec) {
+  const int qa[4] = {x.q.x, x.q.y, x.q.z, x.q.w};
+  const int ka[4] = {x.kv.x, x.kv.y, x.kv.z, x.kv.w};
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    if (j < x.n) {
+      const int64_t l = qa[j], c = ka[j];
+      skv += c;
+      bad |= (l < 1) | (c < 1) | (dec ? (l != 1) : (c < l));
+      if (!dec) {
+        sq += l;
+        const int64_t lc = l * c;
+        if (c == l) seq += lc; else sne += lc;
+        mlc = max(mlc, lc);
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) attention_cost_kernel_u(
@@ -128,7 +79,6 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_u(
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t hd = (int64_t)prm.num_query_heads * prm.head_dim;
-  const double hdd = (double)hd;
   fs_cost_ctx h;
   h.peak_flops = prm.peak_flops; h.mem_bw = prm.mem_bw; h.kernel_overhead_us = prm.kernel_overhead_us;
   h.tp = h.ep = h.moe_tp = h.pp = 1;
@@ -144,53 +94,61 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_u(
       dv[u] = valid ? __ldg(dec + b) != 0 : false;
       fast[u] = (o0[u] & 3) == 0 && o1[u] - o0[u] <= 128;
     }
-    int4 qv[kU], kvv[kU];
-    int nh[kU];
+    Lanes4 x[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
       const int64_t i = o0[u] + 4 * lane;
-      nh[u] = 0;
-      qv[u] = make_int4(0, 0, 0, 0);
-      kvv[u] = make_int4(0, 0, 0, 0);
+      x[u].n = 0;
+      x[u].q = make_int4(0, 0, 0, 0);
+      x[u].kv = make_int4(0, 0, 0, 0);
       if (fast[u] && i < o1[u]) {
-        nh[u] = (int)min((int64_t)4, o1[u] - i);
-        if (nh[u] == 4) {
-          qv[u] = __ldg(reinterpret_cast<const int4*>(q + i));
-          kvv[u] = __ldg(reinterpret_cast<const int4*>(kv + i));
+        x[u].n = (int)min((int64_t)4, o1[u] - i);
+        if (x[u].n == 4) {
+          x[u].q = __ldg(reinterpret_cast<const int4*>(q + i));
+          x[u].kv = __ldg(reinterpret_cast<const int4*>(kv + i));
         } else {
-          qv[u].x = __ldg(q + i); kvv[u].x = __ldg(kv + i);
-          if (nh[u] > 1) { qv[u].y = __ldg(q + i + 1); kvv[u].y = __ldg(kv + i + 1); }
-          if (nh[u] > 2) { qv[u].z = __ldg(q + i + 2); kvv[u].z = __ldg(kv + i + 2); }
+          x[u].q.x = __ldg(q + i); x[u].kv.x = __ldg(kv + i);
+          if (x[u].n > 1) { x[u].q.y = __ldg(q + i + 1); x[u].kv.y = __ldg(kv + i + 1); }
+          if (x[u].n > 2) { x[u].q.z = __ldg(q + i + 2); x[u].kv.z = __ldg(kv + i + 2); }
         }
       }
     }
+    int64_t r_sq[kU], r_skv[kU], r_n[kU];
+    double r_fl[kU];
+    int r_st[kU];
 #pragma unroll
     for (int u = 0; u < kU; u++) {
-      const int64_t b = g + u;
-      if (b >= nb) break;  // uniform across the warp
-      AttnAcc a = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0};
+      int64_t sq = 0, skv = 0, seq = 0, sne = 0, mlc = 0;
+      int bad = 0;
       if (fast[u]) {
-        acc_from_int4(a, qv[u], kvv[u], nh[u], dv[u], hdd);
+        acc4(sq, skv, seq, sne, mlc, bad, x[u], dv[u]);
       } else {
-        for (int64_t i = o0[u] + lane; i < o1[u]; i += 32)
-          attn_acc(a, __ldg(q + i), __ldg(kv + i), dv[u], hdd);
+        for (int64_t i0 = o0[u] + 4 * lane; i0 < o1[u]; i0 += 128) {
+          Lanes4 y;
+          y.n = (int)min((int64_t)4, o1[u] - i0);
+          int qa[4] = {0, 0, 0, 0}, ka[4] = {0, 0, 0, 0};
+          for (int j = 0; j < y.n; j++) { qa[j] = __ldg(q + i0 + j); ka[j] = __ldg(kv + i0 + j); }
+          y.q = make_int4(qa[0], qa[1], qa[2], qa[3]);
+          y.kv = make_int4(ka[0], ka[1], ka[2], ka[3]);
+          acc4(sq, skv, seq, sne, mlc, bad, y, dv[u]);
+        }
       }
-      const int64_t sq = warp_sum_i64(a.sq), skv = warp_sum_i64(a.skv);
-      const int bad = __any_sync(FS_FULL, a.bad_q | a.bad_kv | (dv[u] ? a.bad_dec : a.bad_pre));
-      int st = FS_OK;
-      if (o1[u] <= o0[u]) st = FS_ERR_EMPTY_BATCH;
-      else if (bad) st = FS_ERR_VALUE;
+      skv = warp_sum_i64(skv);
+      bad = __any_sync(FS_FULL, bad);
       double flops;
       if (dv[u]) {
+        sq = o1[u] - o0[u];  // every q is 1 unless `bad`
         flops = attention_decode_flops(skv, hd);
       } else {
-        const int64_t s_eq = warp_sum_i64(a.s_eq), s_ne = warp_sum_i64(a.s_ne);
-        double mt = a.max_term;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) mt = fmax(mt, __shfl_xor_sync(FS_FULL, mt, o));
-        const double total_est = 4.0 * hdd * (double)s_ne + 2.0 * hdd * (double)s_eq;
-        if (mt < kTwo53 * 0.5 && total_est < kTwo53 * 0.5) {
-          flops = i2d(4 * hd * s_ne + 2 * hd * s_eq);  // exact integer sum == sequential fp64 sum
+        sq = warp_sum_i64(sq);
+        seq = warp_sum_i64(seq);
+        sne = warp_sum_i64(sne);
+        mlc = warp_max_i64(mlc);
+        // each term 4*l*c*hd and the total are exact integers below 2^53: the
+        // sequential fp64 sum equals the integer sum in any order
+        const double est = 4.0 * (double)hd * ((double)sne + 0.5 * (double)seq);
+        if (4.0 * (double)mlc * (double)hd < kTwo53 * 0.5 && est < kTwo53 * 0.5) {
+          flops = i2d(4 * hd * sne + 2 * hd * seq);
         } else {
           double tot = 0.0;  // sequential, member order (analytic.py:37-43)
           if (lane == 0)
@@ -198,12 +156,26 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_u(
           flops = __shfl_sync(FS_FULL, tot, 0);
         }
       }
-      if (lane == u) {
-        const double us = attention_us_from(flops, sq, skv, prm.num_query_heads,
-                                            prm.num_kv_heads, prm.head_dim, h, prm.dtype_bytes);
-        out[b] = st == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
-        if (status) status[b] = st;
-      }
+      r_sq[u] = sq;
+      r_skv[u] = skv;
+      r_n[u] = o1[u] - o0[u];
+      r_fl[u] = flops;
+      r_st[u] = bad ? FS_ERR_VALUE : FS_OK;
+    }
+    // lane u finishes batch u
+    int64_t msq = 0, mskv = 0, mn = 0;
+    double mfl = 0.0;
+    int mst = 0;
+#pragma unroll
+    for (int u = 0; u < kU; u++)
+      if (lane == u) { msq = r_sq[u]; mskv = r_skv[u]; mn = r_n[u]; mfl = r_fl[u]; mst = r_st[u]; }
+    const int64_t b = g + lane;
+    if (lane < kU && b < nb) {
+      if (mn <= 0) mst = FS_ERR_EMPTY_BATCH;
+      const double us = attention_us_from(mfl, msq, mskv, prm.num_query_heads, prm.num_kv_heads,
+                                          prm.head_dim, h, prm.dtype_bytes);
+      out[b] = mst == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
+      if (status) status[b] = mst;
     }
   }
 }
