@@ -12,6 +12,8 @@
 //  seeds_kernel            derive_router_seed (orchestrator/base.py:63-65).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "fs_device.cuh"
 #include "fs_engine.h"
 #include "fs_route.cuh"
@@ -180,11 +182,87 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_u(
   }
 }
 
+// Thread per batch: each thread streams its own batch's (q, kv) lengths with
+// 128-bit loads (scalar head/tail to the 16-byte boundary) and accumulates in
+// registers -- no cross-lane reduction at all, so a 72-request batch costs a
+// few dozen instructions per warp-batch-slot. Offsets, phases and outputs are
+// coalesced across the warp; the per-thread length streams are uncoalesced
+// but every 32-byte sector is fully used through L1/L2, so DRAM traffic stays
+// at the algorithmic bytes.
+__global__ void __launch_bounds__(256) attention_cost_kernel_tpb(
+    const int32_t* __restrict__ q, const int32_t* __restrict__ kv,
+    const int64_t* __restrict__ off, const uint8_t* __restrict__ dec, int64_t nb,
+    fs_attn_params prm, double* __restrict__ out, int32_t* __restrict__ status) {
+  const int64_t hd = (int64_t)prm.num_query_heads * prm.head_dim;
+  fs_cost_ctx h;
+  h.peak_flops = prm.peak_flops; h.mem_bw = prm.mem_bw; h.kernel_overhead_us = prm.kernel_overhead_us;
+  h.tp = h.ep = h.moe_tp = h.pp = 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
+    const int64_t o0 = __ldg(off + b), o1 = __ldg(off + b + 1);
+    const bool d = __ldg(dec + b) != 0;
+    int64_t sq = 0, skv = 0, seq = 0, sne = 0, mlc = 0;
+    int bad = 0;
+    int64_t i = o0;
+    const int64_t head_end = min(o1, (o0 + 3) & ~(int64_t)3);
+    for (; i < head_end; i++) {
+      Lanes4 x;
+      x.q = make_int4(__ldg(q + i), 0, 0, 0);
+      x.kv = make_int4(__ldg(kv + i), 0, 0, 0);
+      x.n = 1;
+      acc4(sq, skv, seq, sne, mlc, bad, x, d);
+    }
+    for (; i + 4 <= o1; i += 4) {
+      Lanes4 x;
+      x.q = __ldg(reinterpret_cast<const int4*>(q + i));
+      x.kv = __ldg(reinterpret_cast<const int4*>(kv + i));
+      x.n = 4;
+      acc4(sq, skv, seq, sne, mlc, bad, x, d);
+    }
+    for (; i < o1; i++) {
+      Lanes4 x;
+      x.q = make_int4(__ldg(q + i), 0, 0, 0);
+      x.kv = make_int4(__ldg(kv + i), 0, 0, 0);
+      x.n = 1;
+      acc4(sq, skv, seq, sne, mlc, bad, x, d);
+    }
+    int st = o1 <= o0 ? FS_ERR_EMPTY_BATCH : (bad ? FS_ERR_VALUE : FS_OK);
+    double flops;
+    if (d) {
+      sq = o1 - o0;  // every q is 1 unless `bad`
+      flops = attention_decode_flops(skv, hd);
+    } else {
+      const double est = 4.0 * (double)hd * ((double)sne + 0.5 * (double)seq);
+      if (4.0 * (double)mlc * (double)hd < kTwo53 * 0.5 && est < kTwo53 * 0.5) {
+        flops = i2d(4 * hd * sne + 2 * hd * seq);  // exact integer sum == sequential fp64 sum
+      } else {
+        flops = 0.0;  // sequential, member order (analytic.py:37-43)
+        for (int64_t j = o0; j < o1; j++) flops = flops + attention_prefill_term(q[j], kv[j], hd);
+      }
+    }
+    const double us = attention_us_from(flops, sq, skv, prm.num_query_heads, prm.num_kv_heads,
+                                        prm.head_dim, h, prm.dtype_bytes);
+    out[b] = st == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
+    if (status) status[b] = st;
+  }
+}
+
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,
                           const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out,
                           int32_t* status, int n_sms, void* stream) {
   if (nb <= 0) return 0;
   const int threads = 256;
+  if (getenv("FS_C2_WARP") == nullptr) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attention_cost_kernel_tpb, threads, 0);
+    if (per < 1) per = 1;
+    int64_t blocks = (nb + threads - 1) / threads;
+    const int64_t cap = (int64_t)n_sms * per;
+    if (blocks > cap) blocks = cap;
+    attention_cost_kernel_tpb<<<(int)blocks, threads, 0, (cudaStream_t)stream>>>(q, kv, off, dec, nb,
+                                                                                prm, out, status);
+    return 1;
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attention_cost_kernel_u, threads, 0);
   if (per_sm < 1) per_sm = 1;
