@@ -83,10 +83,13 @@ enum fs_status {
   FS_ERR_ROUTING_TIE = 9,          /* exact key tie at the top-k boundary: argpartition's
                                       choice is implementation-defined; flagged, not guessed */
   FS_ERR_UNSUPPORTED = 10,         /* feature not on the device path yet (dirichlet_skew,
-                                      learned cost models)                                 */
+                                      learned grouped GEMM on MoE layers)                  */
   FS_ERR_CAPACITY = 11,            /* engine limit (FS_MAX_*) exceeded                     */
   FS_ERR_INTERNAL = 12,            /* invariant violated inside the engine                 */
-  FS_ERR_VALUE = 13                /* ValueError raised by a cost-model argument check     */
+  FS_ERR_VALUE = 13,               /* ValueError raised by a cost-model argument check     */
+  FS_ERR_SCHEMA = 14               /* costmodel/model.py:118-123, 315-320 SchemaMismatch:
+                                      the model's schema is wrong for its slot; raised at
+                                      the first prediction, like the reference             */
 };
 
 /* Hardware profile + the parallel degrees one OperatorCosts instance uses
@@ -145,9 +148,38 @@ typedef struct {
   int64_t kv_bytes_per_token; /* topology.py:241-243 */
   int64_t max_events;         /* core.py:142 (default 50,000,000) */
   int32_t total_gpus;         /* Deployment.total_gpus */
-  int32_t cost_model_learned; /* 1 when a learned model file is attached (not yet on device) */
+  int32_t attn_forest;        /* learned attention model: index into the forest set, -1 =
+                                 analytic, -2 = model with a wrong schema (FS_ERR_SCHEMA at
+                                 the first prediction); CostModel.predict_attention,
+                                 costmodel/model.py:313-321 */
+  int32_t gg_forest;          /* learned grouped-GEMM model, same encoding
+                                 (CostModel.predict_grouped_gemm, model.py:323-327); on
+                                 the device path for dense FFNs (cluster.py:286-296) */
+  int32_t pad0;
   int64_t est_cost;           /* host estimate used to order the device work queue */
 } fs_instance_desc;
+
+/* Learned operator models (BaggedForest, costmodel/forest.py:46-242): trees as
+ * flat node arrays, children addressed by global node index. */
+typedef struct {
+  int32_t n_trees;
+  int32_t n_features;         /* 17 for attention_v1, 12 for grouped_gemm_v1 */
+  int64_t tree_offset;        /* first entry of this forest in tree_root[] */
+} fs_forest_desc;
+
+typedef struct {
+  const fs_forest_desc* forests;
+  int32_t n_forests;
+  int32_t pad0;
+  const int64_t* tree_root;   /* global node index of each tree's root */
+  int64_t n_trees;
+  const int32_t* feature;     /* split feature, -1 marks a leaf */
+  const double* threshold;    /* go left when x[feature] <= threshold */
+  const int32_t* left;
+  const int32_t* right;
+  const double* value;        /* leaf prediction (us) */
+  int64_t n_nodes;
+} fs_forest_set;
 
 typedef struct {
   const int64_t* arrival_ns;    /* request_order (stable sort by arrival), workload.py:219 */
@@ -256,6 +288,10 @@ int fs_run_batch(fs_engine* e,
                  fs_request_out per_request,       /* members nullable */
                  fs_log* log);                     /* nullable */
 
+/* Stage learned models (kept on the device until replaced); instances refer
+ * to them by index (fs_instance_desc.attn_forest). */
+int fs_set_forests(fs_engine* e, fs_forest_set forests);
+
 /* Resident path: stage inputs once, then launch repeatedly on device data. */
 int fs_stage(fs_engine* e,
              const fs_instance_desc* descs, int32_t n_instances,
@@ -300,6 +336,19 @@ int fs_attention_features_dev(fs_engine* e, const int32_t* q_lens, const int32_t
 int fs_attention_features(fs_engine* e, const int32_t* q_lens, const int32_t* kv_lens,
                           const int64_t* offsets, const uint8_t* is_decode, int64_t n_batches,
                           fs_attn_params params, double* out17);
+
+/* LearnedOperatorModel.predict_us(AttentionFeatures(...).vector()) over CSR
+ * batches with staged forest `forest` (costmodel/model.py:126-136,
+ * forest.py:234-239): 17 features, tree walks, sorted-leaf numpy mean,
+ * max(., 1e-6). Device pointers, async on stream. */
+int fs_attention_forest_dev(fs_engine* e, int32_t forest, const int32_t* q_lens,
+                            const int32_t* kv_lens, const int64_t* offsets,
+                            const uint8_t* is_decode, int64_t n_batches, fs_attn_params params,
+                            double* out_us, void* stream);
+/* Same, host buffers (synchronous). */
+int fs_attention_forest(fs_engine* e, int32_t forest, const int32_t* q_lens,
+                        const int32_t* kv_lens, const int64_t* offsets, const uint8_t* is_decode,
+                        int64_t n_batches, fs_attn_params params, double* out_us);
 
 /* route_tokens(T, E, k, "uniform", seed) for a list of calls (host buffers).
  * counts_out: n_calls x num_experts int32. status: per call. */

@@ -260,6 +260,7 @@ typedef struct Sim {
   const fs_instance_desc* d;
   const fs_seed_prefix* prefixes;
   const int64_t* trace_counts;
+  const fs_forest_set* forests;
   int N, R;
   const int64_t* arrival;
   const int32_t* prompt;
@@ -441,6 +442,86 @@ static double grouped_gemm_us(Sim* s, const int64_t* counts, int n, int64_t d_mo
   return roofline_us(flops, (double)(wb + ab), h);
 }
 
+/* ---- learned attention model (features.py:23-32,101-115; forest.py:67-78,234-239;
+ *      model.py:126-133) ---- */
+/* numpy's pairwise summation of a contiguous float64 array (DOUBLE_pairwise_sum):
+ * plain loop below 8 elements, 8 accumulators up to 128, recursive halving above */
+static double np_pairwise(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; i++) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; j++) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; i++) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+/* _stats(values): sum, sum_sq, max, min, mean, std (ddof 0) */
+static void np_stats(const int64_t* v, int n, double out[6]) {
+  double* a = (double*)malloc(sizeof(double) * (size_t)n);
+  double* sq = (double*)malloc(sizeof(double) * (size_t)n);
+  double mx = (double)v[0], mn = (double)v[0];
+  for (int i = 0; i < n; i++) {
+    a[i] = (double)v[i];
+    sq[i] = a[i] * a[i];
+    if (a[i] > mx) mx = a[i];
+    if (a[i] < mn) mn = a[i];
+  }
+  double sum = np_pairwise(a, n);
+  double mean = sum / (double)n;
+  for (int i = 0; i < n; i++) { double x = a[i] - mean; sq[i] = x * x; }
+  double var = np_pairwise(sq, n) / (double)n;
+  for (int i = 0; i < n; i++) sq[i] = a[i] * a[i];
+  out[0] = sum;
+  out[1] = np_pairwise(sq, n);
+  out[2] = mx;
+  out[3] = mn;
+  out[4] = mean;
+  out[5] = sqrt(var);
+  free(a);
+  free(sq);
+}
+/* AttentionFeatures.vector() */
+static void attention_features(int decode, const int64_t* q, const int64_t* kv, int B, int hq,
+                               int hkv, int hdim, double x[17]) {
+  x[0] = decode ? 1.0 : 0.0;
+  x[1] = (double)B;
+  np_stats(q, B, x + 2);
+  np_stats(kv, B, x + 8);
+  x[14] = (double)hq;
+  x[15] = (double)hkv;
+  x[16] = (double)hdim;
+}
+static int cmp_dbl(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+/* np.maximum(np.sort(per_tree).mean(), 1e-6) */
+static double forest_predict(const fs_forest_set* fs, int forest, const double* x) {
+  const fs_forest_desc* f = &fs->forests[forest];
+  double* vals = (double*)malloc(sizeof(double) * (size_t)f->n_trees);
+  for (int t = 0; t < f->n_trees; t++) {
+    int64_t node = fs->tree_root[f->tree_offset + t];
+    while (fs->feature[node] >= 0)
+      node = (x[fs->feature[node]] <= fs->threshold[node]) ? fs->left[node] : fs->right[node];
+    vals[t] = fs->value[node];
+  }
+  qsort(vals, (size_t)f->n_trees, sizeof(double), cmp_dbl);
+  double mean = np_pairwise(vals, f->n_trees) / (double)f->n_trees;
+  free(vals);
+  return mean < 1e-6 ? 1e-6 : mean;
+}
+
 /* ---- route_tokens (routing.py:65-113) ---- */
 static int64_t* route(Sim* s, int64_t T, uint32_t seed, int policy_uniform_forced,
                       int rep, int mb, int64_t step, int layer) {
@@ -584,18 +665,47 @@ static double tpcoll_us(const fs_instance_desc* d, const fs_cost_ctx* c, int64_t
 }
 static double attn_us(Sim* s, const fs_cost_ctx* c, const Plan* p) {
   const fs_instance_desc* d = s->d;
-  if (d->cost_model_learned) fail(s, FS_ERR_UNSUPPORTED, 100);
   int hq, hkv; heads(d, c->tp, &hq, &hkv);
   int64_t* q = (int64_t*)malloc(sizeof(int64_t) * (size_t)p->n * 2);
   int64_t* kv = q + p->n;
   plan_lengths(s, p, q, kv);
-  double v = attention_us_analytic(p->phase == 1, q, kv, p->n, hq, hkv, d->head_dim, c, d->dtype_bytes);
+  double v;
+  if (d->attn_forest != -1) {
+    /* CostModel.predict_attention raises SchemaMismatch for a non-attention_v1
+     * model at its first prediction (costmodel/model.py:313-320) */
+    if (d->attn_forest < 0) { free(q); fail(s, FS_ERR_SCHEMA, 0); }
+    if (!s->forests || d->attn_forest >= s->forests->n_forests) { free(q); fail(s, FS_ERR_INTERNAL, 7); }
+    double x[17];
+    attention_features(p->phase == 1, q, kv, p->n, hq, hkv, d->head_dim, x);
+    v = forest_predict(s->forests, d->attn_forest, x);
+  } else {
+    v = attention_us_analytic(p->phase == 1, q, kv, p->n, hq, hkv, d->head_dim, c, d->dtype_bytes);
+  }
   free(q);
   return v;
 }
 static double dense_ffn_us(Sim* s, const fs_cost_ctx* c, int64_t n) {
   const fs_instance_desc* d = s->d;
   int64_t dff = d->d_ff / c->tp; if (dff < 1) dff = 1;
+  if (d->gg_forest != -1) {
+    /* OperatorCosts.ffn_us for a dense model (cluster.py:286-296) with a learned
+     * grouped-GEMM model: GroupedGemmFeatures(n, (n,), d_model, dff, 1, "local")
+     * .vector() (features.py:166-209) -- one expert holding every token */
+    if (d->gg_forest < 0) fail(s, FS_ERR_SCHEMA, 0);  /* check_schema, model.py:325 */
+    if (!s->forests || d->gg_forest >= s->forests->n_forests) fail(s, FS_ERR_INTERNAL, 7);
+    if (n < 1) fail(s, FS_ERR_EMPTY_BATCH, 2);
+    const double cn = (double)n;
+    const double active_mean = cn / 1.0, mean = cn / 1.0;
+    const double dev = cn - mean;
+    const double std = sqrt((dev * dev) / 1.0);
+    double x[12] = {cn, 1.0, (double)d->d_model, (double)dff, 1.0,
+                    1.0 / 1.0,            /* expert_selection_ratio */
+                    cn / active_mean,     /* load_max_over_mean */
+                    std / mean,           /* load_cv (mean > 0) */
+                    1.0,                  /* load_entropy: single expert */
+                    cn, mean, std};
+    return forest_predict(s->forests, d->gg_forest, x);
+  }
   int64_t counts[1] = {n};
   return grouped_gemm_us(s, counts, 1, d->d_model, dff, d->ffn_matrices, c, d->dtype_bytes);
 }
@@ -1143,7 +1253,7 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
                      const int64_t* arrival, const int32_t* prompt, const int32_t* output,
                      const int32_t* id_rank, fs_metric_row* row, fs_replica_out* rep_out,
                      int64_t* first_ns, int64_t* done_ns, int32_t* done_rank,
-                     fs_log* log, int inst) {
+                     fs_log* log, int inst, const fs_forest_set* forests) {
   Sim S;
   Sim* s = &S;
   memset(s, 0, sizeof S);
@@ -1154,6 +1264,7 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
   s->R = d->n_replicas;
   s->arrival = arrival; s->prompt = prompt; s->output = output; s->id_rank = id_rank;
   s->log = log; s->inst = inst;
+  s->forests = forests;
   int N = s->N, R = s->R;
   s->emitted = (int32_t*)calloc((size_t)N + 1, sizeof(int32_t));
   s->first_ns = first_ns; s->done_ns = done_ns; s->done_rank = done_rank;
@@ -1174,6 +1285,8 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
   if (log && log->batch_count) { log->batch_count[inst] = 0; log->route_count[inst] = 0; log->truncated[inst] = 0; }
 
   if (setjmp(s->jb) == 0) {
+    /* learned grouped GEMM on MoE layers needs numpy's np.log (entropy): next */
+    if (d->has_moe && d->gg_forest != -1) fail(s, FS_ERR_UNSUPPORTED, 101);
     /* schedule_arrivals (base.py:167-177): seq 0..N-1 */
     for (int i = 0; i < N; i++) schedule(s, arrival[i], EV_ARRIVAL, -1, i);
     while (s->hn) {
@@ -1336,7 +1449,7 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
 typedef struct {
   const fs_instance_desc* descs; const fs_replica_desc* reps; const fs_seed_prefix* pf;
   const int64_t* tc; fs_request_soa rq; fs_metric_row* rows; fs_replica_out* ro;
-  fs_request_out pr; fs_log* log; int n; int next; pthread_mutex_t mu;
+  fs_request_out pr; fs_log* log; const fs_forest_set* forests; int n; int next; pthread_mutex_t mu;
 } Job;
 static void* worker(void* arg) {
   Job* j = (Job*)arg;
@@ -1355,7 +1468,7 @@ static void* worker(void* arg) {
     fs_replica_out* ro = j->ro ? j->ro + d->replica_offset : tmp;
     fso_run_instance(d, j->reps + d->replica_offset, j->pf, j->tc, j->rq.arrival_ns + o,
                      j->rq.prompt_tokens + o, j->rq.output_tokens + o, j->rq.id_rank + o,
-                     &j->rows[i], ro, fn, dn, dr, j->log, i);
+                     &j->rows[i], ro, fn, dn, dr, j->log, i, j->forests);
     if (!j->pr.first_token_ns) free(fn);
     if (!j->pr.done_ns) free(dn);
     if (!j->pr.completion_rank) free(dr);
@@ -1367,11 +1480,13 @@ int fso_run_batch(const fs_instance_desc* descs, int32_t n_instances,
                   const fs_replica_desc* replicas, const fs_seed_prefix* prefixes,
                   const int64_t* trace_counts, fs_request_soa requests,
                   fs_metric_row* rows_out, fs_replica_out* replica_out,
-                  fs_request_out per_request, fs_log* log, int threads) {
+                  fs_request_out per_request, fs_log* log, int threads,
+                  const fs_forest_set* forests) {
   Job j;
   memset(&j, 0, sizeof j);
   j.descs = descs; j.reps = replicas; j.pf = prefixes; j.tc = trace_counts; j.rq = requests;
   j.rows = rows_out; j.ro = replica_out; j.pr = per_request; j.log = log; j.n = n_instances;
+  j.forests = forests;
   pthread_mutex_init(&j.mu, NULL);
   if (threads < 1) threads = 1;
   if (threads > 512) threads = 512;
@@ -1447,6 +1562,12 @@ double fso_linear_us(int64_t m, int64_t n, int64_t k, double peak, double bw, do
   fs_cost_ctx c = {peak, bw, ovh, 1, 1, 1, 1};
   return linear_us(m, n, k, &c, dt);
 }
+/* LearnedOperatorModel.predict_us on one attention batch (for golden tests) */
+double fso_attention_forest(const fs_forest_set* fs, int forest, int decode, const int64_t* q,
+                            const int64_t* kv, int B, int hq, int hkv, int hdim, double* x17) {
+  attention_features(decode, q, kv, B, hq, hkv, hdim, x17);
+  return forest_predict(fs, forest, x17);
+}
 double fso_pysum(const double* x, int n) {
   pysum_t s;
   pysum_init(&s);
@@ -1459,7 +1580,7 @@ int fso_struct_sizes(int64_t* out, int n) {
                        (int64_t)sizeof(fs_replica_desc), (int64_t)sizeof(fs_instance_desc),
                        (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
                        (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
-                       (int64_t)sizeof(fs_attn_params)};
+                       (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc)};
   const int k = (int)(sizeof(s) / sizeof(s[0]));
   for (int i = 0; i < n && i < k; i++) out[i] = s[i];
   return k;

@@ -15,6 +15,7 @@ import subprocess
 import numpy as np
 
 from paper_2508_03148_b200 import abi
+from paper_2508_03148_b200.costmodel import forest_set_struct
 from paper_2508_03148_b200.engine import LogSpec, RawResults, alloc_results, make_log, soa
 from paper_2508_03148_b200.lower import Lowered
 
@@ -38,7 +39,7 @@ def load():
     vp = ctypes.c_void_p
     lib.fso_run_batch.restype = ctypes.c_int
     lib.fso_run_batch.argtypes = [vp, ctypes.c_int32, vp, vp, vp, abi.RequestSoA, vp, vp,
-                                  abi.RequestOut, vp, ctypes.c_int]
+                                  abi.RequestOut, vp, ctypes.c_int, vp]
     lib.fso_router_seed.restype = ctypes.c_uint32
     lib.fso_router_seed.argtypes = [vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int32]
     lib.fso_routing_key.restype = None
@@ -52,6 +53,9 @@ def load():
                                      ctypes.c_double, ctypes.c_int]
     lib.fso_linear_us.restype = ctypes.c_double
     lib.fso_linear_us.argtypes = [ctypes.c_int64] * 3 + [ctypes.c_double] * 3 + [ctypes.c_int]
+    lib.fso_attention_forest.restype = ctypes.c_double
+    lib.fso_attention_forest.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
     lib.fso_pysum.restype = ctypes.c_double
     lib.fso_pysum.argtypes = [vp, ctypes.c_int]
     abi.check_sizes(lib, "fso_struct_sizes")
@@ -65,10 +69,12 @@ def run(low: Lowered, log: LogSpec | None = None, threads: int = 1) -> RawResult
     if log is not None:
         res.log = make_log(low.n_instances, log)
     pr = abi.RequestOut(abi.ptr(res.first_ns), abi.ptr(res.done_ns), abi.ptr(res.done_rank))
+    fset = forest_set_struct(low.forests) if low.forests is not None else None
     lib.fso_run_batch(abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas),
                       abi.ptr(low.prefixes), abi.ptr(low.trace_counts), soa(low),
                       abi.ptr(res.rows), abi.ptr(res.replica_out), pr,
-                      ctypes.byref(res.log.c_struct) if res.log is not None else None, threads)
+                      ctypes.byref(res.log.c_struct) if res.log is not None else None, threads,
+                      ctypes.byref(fset) if fset is not None else None)
     return res
 
 
@@ -95,6 +101,18 @@ def attention_us(decode: bool, q, kv, hq, hkv, hd, peak, bw, ovh=5.0, dt=2) -> f
     kv = np.ascontiguousarray(kv, dtype=np.int64)
     return load().fso_attention_us(int(decode), abi.ptr(q), abi.ptr(kv), len(q), hq, hkv, hd,
                                    peak, bw, ovh, dt)
+
+
+def attention_forest(forests, forest: int, decode: bool, q, kv, hq: int, hkv: int, hd: int):
+    """(prediction_us, features[17]) for one batch: AttentionFeatures.vector() and
+    LearnedOperatorModel.predict_us (costmodel/features.py:101-115, model.py:126-136)."""
+    q = np.ascontiguousarray(q, dtype=np.int64)
+    kv = np.ascontiguousarray(kv, dtype=np.int64)
+    x = np.zeros(17, dtype=np.float64)
+    fset = forest_set_struct(forests)
+    v = load().fso_attention_forest(ctypes.byref(fset), forest, int(decode), abi.ptr(q),
+                                    abi.ptr(kv), len(q), hq, hkv, hd, abi.ptr(x))
+    return v, x
 
 
 def pysum(xs) -> float:

@@ -15,6 +15,7 @@ MAX_EXPERTS = 1024
 MAX_TOPK = 16
 MAX_MICRO_BATCHES = 64
 MAX_REPLICAS = 64
+MAX_FOREST_TREES = 256  # fs_forest.cuh kMaxForestTrees (per-warp leaf sort in shared memory)
 DEFAULT_MAX_EVENTS = 50_000_000
 
 MODE = {"colocated": 0, "pd": 1, "af": 2}
@@ -50,7 +51,8 @@ INSTANCE_DESC = np.dtype([
     ("intra_latency_s", "<f8"), ("intra_bandwidth_bps", "<f8"),
     ("inter_latency_s", "<f8"), ("inter_bandwidth_bps", "<f8"),
     ("kv_bytes_per_token", "<i8"), ("max_events", "<i8"),
-    ("total_gpus", "<i4"), ("cost_model_learned", "<i4"), ("est_cost", "<i8"),
+    ("total_gpus", "<i4"), ("attn_forest", "<i4"), ("gg_forest", "<i4"), ("pad0", "<i4"),
+    ("est_cost", "<i8"),
 ], align=True)
 
 METRIC_ROW = np.dtype([
@@ -80,13 +82,25 @@ ATTN_PARAMS = np.dtype([("num_query_heads", "<i4"), ("num_kv_heads", "<i4"), ("h
                         ("dtype_bytes", "<i4"), ("peak_flops", "<f8"), ("mem_bw", "<f8"),
                         ("kernel_overhead_us", "<f8")], align=True)
 
+FOREST_DESC = np.dtype([("n_trees", "<i4"), ("n_features", "<i4"), ("tree_offset", "<i8")],
+                       align=True)
+
 STRUCT_ORDER = (COST_CTX, SEED_PREFIX, REPLICA_DESC, INSTANCE_DESC, METRIC_ROW, REPLICA_OUT,
-                BATCH_REC, ROUTE_REC, ATTN_PARAMS)
+                BATCH_REC, ROUTE_REC, ATTN_PARAMS, FOREST_DESC)
 
 
 class RequestSoA(ctypes.Structure):
     _fields_ = [("arrival_ns", ctypes.c_void_p), ("prompt_tokens", ctypes.c_void_p),
                 ("output_tokens", ctypes.c_void_p), ("id_rank", ctypes.c_void_p)]
+
+
+class ForestSetC(ctypes.Structure):
+    _fields_ = [("forests", ctypes.c_void_p), ("n_forests", ctypes.c_int32),
+                ("pad0", ctypes.c_int32), ("tree_root", ctypes.c_void_p),
+                ("n_trees", ctypes.c_int64), ("feature", ctypes.c_void_p),
+                ("threshold", ctypes.c_void_p), ("left", ctypes.c_void_p),
+                ("right", ctypes.c_void_p), ("value", ctypes.c_void_p),
+                ("n_nodes", ctypes.c_int64)]
 
 
 class RequestOut(ctypes.Structure):

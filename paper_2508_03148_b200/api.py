@@ -13,6 +13,7 @@ import time
 from dataclasses import dataclass
 
 from .config import DeploymentConfig, parse_config
+from .costmodel import check_model_slots_engine
 from .engine import Engine, LogSpec, default_engine
 from .lower import InstanceSpec, Lowered, lower
 from .metrics import InstanceResult, MetricsBundle, compute_metrics, split_results
@@ -31,11 +32,12 @@ class Failure:
 
 def instance_spec(config: DeploymentConfig) -> InstanceSpec:
     """What `run_one` builds before `make_simulation` (cli.py:84-94)."""
-    cm = config.cost_model
+    attention_model, grouped_model = config.cost_model.load_models()
+    check_model_slots_engine(attention_model, grouped_model)
     return InstanceSpec(
         deployment=config.deployment(), requests=config.request_arrays(), policy=config.policy,
         af=config.af if config.mode == "af" else None, routing=config.routing, seed=config.seed,
-        learned=bool(cm.attention_model_path or cm.grouped_gemm_model_path))
+        attention_model=attention_model, grouped_gemm_model=grouped_model)
 
 
 @dataclass
@@ -82,8 +84,9 @@ def run_one(config: DeploymentConfig, engine: Engine | None = None) -> dict:
     from .orchestrator import make_simulation
     spec = instance_spec(config)
     sim = make_simulation(config.mode, spec.deployment, spec.requests.to_requests(), spec.policy,
-                          af=spec.af, routing=spec.routing, seed=spec.seed, engine=engine)
-    sim.spec.learned = spec.learned
+                          af=spec.af, routing=spec.routing, seed=spec.seed,
+                          attention_model=spec.attention_model,
+                          grouped_gemm_model=spec.grouped_gemm_model, engine=engine)
     result = sim.run()
     return {"config": config, "trace": result, "metrics": compute_metrics(result),
             "config_hash": config.config_hash()}

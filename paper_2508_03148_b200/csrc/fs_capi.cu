@@ -54,6 +54,10 @@ struct fs_engine {
   // cost-model scratch
   DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
       c_layers, c_seeds, c_pf, c_mid;
+  // learned models (persist across stages)
+  DevBuf f_descs, f_roots, f_feature, f_threshold, f_left, f_right, f_value;
+  fs::ForestView fv{};
+  bool learned = false;  // staged batch uses the learned simulation variant
   int32_t n_inst = 0, n_reps = 0, n_prefixes = 0;
   int64_t n_req = 0;
   int staged = 0;
@@ -88,7 +92,7 @@ int fs_struct_sizes(int64_t* out, int n) {
                        (int64_t)sizeof(fs_replica_desc), (int64_t)sizeof(fs_instance_desc),
                        (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
                        (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
-                       (int64_t)sizeof(fs_attn_params)};
+                       (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc)};
   const int k = (int)(sizeof(s) / sizeof(s[0]));
   for (int i = 0; i < n && i < k; i++) out[i] = s[i];
   return k;
@@ -240,7 +244,18 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   P.inst_cycles = e->cycles.as<int64_t>();
   P.log_enabled = 0;
   // routing job board: one slot per resident warp of the persistent grid
-  P.n_slots = fs::simulation_slots(e->n_sms, n_instances);
+  e->learned = false;
+  for (int i = 0; i < n_instances; i++) {
+    const int32_t fsel[2] = {descs[i].attn_forest, descs[i].gg_forest};
+    for (int32_t f : fsel) {
+      if (f >= e->fv.n_forests || f < -2) {
+        e->err = "instance " + std::to_string(i) + ": forest index not staged (fs_set_forests)";
+        return 13;
+      }
+      if (f != -1) e->learned = true;
+    }
+  }
+  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned);
   int max_e = 0;
   for (int i = 0; i < n_instances; i++)
     if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);
@@ -248,6 +263,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   FS_CHECK(e->inst_done.ensure(2 * sizeof(int32_t)));
   P.inst_done = e->inst_done.as<int32_t>();
   P.open_jobs = e->inst_done.as<int32_t>() + 1;
+  P.fv = e->fv;
   if (max_e > 0) {
     FS_CHECK(e->jobs.ensure((size_t)P.n_slots * sizeof(fs::RouteJob)));
     FS_CHECK(e->job_counts.ensure((size_t)P.n_slots * fs::kJobLayers * P.job_max_e * 4));
@@ -276,7 +292,7 @@ int fs_launch_async(fs_engine* e, void* stream) {
   if (e->params.jobs)
     FS_CHECK(cudaMemsetAsync(e->jobs.p, 0, (size_t)e->params.n_slots * sizeof(fs::RouteJob), s));
   e->last_launches = 0;
-  e->last_launches += fs::launch_simulation(e->params, e->n_sms, s);
+  e->last_launches += fs::launch_simulation(e->params, e->learned, s);
   e->last_launches += fs::launch_metrics(e->params, s);
   FS_CHECK(cudaGetLastError());
   return 0;
@@ -464,6 +480,76 @@ int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds,
   FS_CHECK(cudaMemcpyAsync(counts_out, e->c_counts.p, 4 * (size_t)n_calls * num_experts,
                            cudaMemcpyDeviceToHost, s));
   FS_CHECK(cudaMemcpyAsync(status, e->c_status.p, 4 * (size_t)n_calls, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fs_set_forests(fs_engine* e, fs_forest_set f) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  for (int i = 0; i < f.n_forests; i++) {
+    const fs_forest_desc& d = f.forests[i];
+    if (d.n_trees < 1 || d.n_trees > fs::kMaxForestTrees || d.tree_offset < 0 ||
+        d.tree_offset + d.n_trees > f.n_trees) {
+      e->err = "forest " + std::to_string(i) + ": bad tree range (1 <= n_trees <= 256)";
+      return 12;
+    }
+  }
+  FS_CHECK(upload(e->f_descs, f.forests, (size_t)f.n_forests, s));
+  FS_CHECK(upload(e->f_roots, f.tree_root, (size_t)f.n_trees, s));
+  FS_CHECK(upload(e->f_feature, f.feature, (size_t)f.n_nodes, s));
+  FS_CHECK(upload(e->f_threshold, f.threshold, (size_t)f.n_nodes, s));
+  FS_CHECK(upload(e->f_left, f.left, (size_t)f.n_nodes, s));
+  FS_CHECK(upload(e->f_right, f.right, (size_t)f.n_nodes, s));
+  FS_CHECK(upload(e->f_value, f.value, (size_t)f.n_nodes, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  e->fv.forests = e->f_descs.as<fs_forest_desc>();
+  e->fv.n_forests = f.n_forests;
+  e->fv.tree_root = e->f_roots.as<int64_t>();
+  e->fv.feature = e->f_feature.as<int32_t>();
+  e->fv.threshold = e->f_threshold.as<double>();
+  e->fv.left = e->f_left.as<int32_t>();
+  e->fv.right = e->f_right.as<int32_t>();
+  e->fv.value = e->f_value.as<double>();
+  e->params.fv = e->fv;
+  return 0;
+}
+
+int fs_attention_forest_dev(fs_engine* e, int32_t forest, const int32_t* q_lens,
+                            const int32_t* kv_lens, const int64_t* offsets,
+                            const uint8_t* is_decode, int64_t n_batches, fs_attn_params params,
+                            double* out_us, void* stream) {
+  if (!e) return 1;
+  if (forest < 0 || forest >= e->fv.n_forests) {
+    e->err = "forest index out of range (stage models with fs_set_forests)";
+    return 13;
+  }
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+  e->last_launches = fs::launch_attention_forest(e->fv, forest, q_lens, kv_lens, offsets, is_decode,
+                                                 n_batches, params, out_us, e->n_sms, s);
+  FS_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int fs_attention_forest(fs_engine* e, int32_t forest, const int32_t* q_lens, const int32_t* kv_lens,
+                        const int64_t* offsets, const uint8_t* is_decode, int64_t n_batches,
+                        fs_attn_params params, double* out_us) {
+  if (!e) return 1;
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  const int64_t n_el = n_batches > 0 ? offsets[n_batches] : 0;
+  FS_CHECK(upload(e->c_q, q_lens, (size_t)n_el, s));
+  FS_CHECK(upload(e->c_kv, kv_lens, (size_t)n_el, s));
+  FS_CHECK(upload(e->c_off, offsets, (size_t)n_batches + 1, s));
+  FS_CHECK(upload(e->c_dec, is_decode, (size_t)n_batches, s));
+  FS_CHECK(e->c_out.ensure((size_t)std::max<int64_t>(n_batches, 1) * 8));
+  int rc = fs_attention_forest_dev(e, forest, e->c_q.as<int32_t>(), e->c_kv.as<int32_t>(),
+                                   e->c_off.as<int64_t>(), e->c_dec.as<uint8_t>(), n_batches,
+                                   params, e->c_out.as<double>(), s);
+  if (rc) return rc;
+  FS_CHECK(cudaMemcpyAsync(out_us, e->c_out.p, 8 * n_batches, cudaMemcpyDeviceToHost, s));
   FS_CHECK(cudaStreamSynchronize(s));
   return 0;
 }

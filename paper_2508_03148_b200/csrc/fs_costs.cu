@@ -424,3 +424,55 @@ int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int
 }
 
 }  // namespace fs
+
+namespace fs {
+
+// C2 in learned mode: LearnedOperatorModel.predict_us(AttentionFeatures(...).vector())
+// per CSR batch, one warp per batch (features by lanes, one tree per lane).
+constexpr int kForestWarps = 4;
+
+__global__ void __launch_bounds__(32 * kForestWarps) attention_forest_kernel(
+    ForestView fv, int forest, const int32_t* __restrict__ q, const int32_t* __restrict__ kv,
+    const int64_t* __restrict__ off, const uint8_t* __restrict__ dec, int64_t nb,
+    fs_attn_params prm, double* __restrict__ out) {
+  __shared__ double sx[kForestWarps][17];
+  __shared__ double svals[kForestWarps][kMaxForestTrees];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = (int64_t)blockIdx.x * kForestWarps + w;
+  const int64_t nwarps = (int64_t)gridDim.x * kForestWarps;
+  for (int64_t b = warp; b < nb; b += nwarps) {
+    const int64_t o0 = off[b], n = off[b + 1] - o0;
+    const bool d = dec[b] != 0;
+    auto fq = [&](int64_t i) -> int64_t { return q[o0 + i]; };
+    auto fk = [&](int64_t i) -> int64_t { return kv[o0 + i]; };
+    double x[17];
+    attention_features_w(d, n, fq, fk, prm.num_query_heads, prm.num_kv_heads, prm.head_dim, lane,
+                         x);
+    if (lane < 17) {
+#pragma unroll
+      for (int j = 0; j < 17; j++)
+        if (j == lane) sx[w][j] = x[j];
+    }
+    __syncwarp();
+    const double v = forest_predict_w(fv, forest, sx[w], svals[w], lane);
+    if (lane == 0) out[b] = v;
+    __syncwarp();
+  }
+}
+
+int launch_attention_forest(const ForestView& fv, int forest, const int32_t* q, const int32_t* kv,
+                            const int64_t* off, const uint8_t* dec, int64_t nb, fs_attn_params prm,
+                            double* out, int n_sms, void* stream) {
+  if (nb <= 0) return 0;
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attention_forest_kernel, 32 * kForestWarps, 0);
+  if (per < 1) per = 1;
+  int64_t blocks = (nb + kForestWarps - 1) / kForestWarps;
+  const int64_t cap = (int64_t)n_sms * per;
+  if (blocks > cap) blocks = cap;
+  attention_forest_kernel<<<(int)blocks, 32 * kForestWarps, 0, (cudaStream_t)stream>>>(
+      fv, forest, q, kv, off, dec, nb, prm, out);
+  return 1;
+}
+
+}  // namespace fs

@@ -3,6 +3,7 @@
 #include <cstdint>
 
 #include "../../include/frontier_b200.h"
+#include "fs_forest.cuh"
 
 namespace fs {
 
@@ -88,12 +89,22 @@ struct EngineParams {
   int32_t job_max_e;
   int32_t* inst_done;            // instances finished (helpers stop at n_inst)
   int32_t* open_jobs;            // published jobs with unclaimed chunks
+  ForestView fv;                 // learned operator models (fs_set_forests)
 };
 
 // host-side launchers (fs_engine.cu / fs_metrics.cu / fs_costs.cu)
 void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void* stream);
-int simulation_slots(int n_sms, int n_inst);
-int launch_simulation(const EngineParams& p, int n_sms, void* stream);
+// simulation kernel variants (fs_sim.cuh compiled twice)
+namespace analytic {
+int slots(int n_sms, int n_inst);
+int launch(const EngineParams& p, void* stream);
+}  // namespace analytic
+namespace learned {
+int slots(int n_sms, int n_inst);
+int launch(const EngineParams& p, void* stream);
+}  // namespace learned
+int simulation_slots(int n_sms, int n_inst, bool learned);
+int launch_simulation(const EngineParams& p, bool learned, void* stream);
 int launch_metrics(const EngineParams& p, void* stream);
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,
                           const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out,
@@ -101,6 +112,9 @@ int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* of
 int launch_attention_features(const int32_t* q, const int32_t* kv, const int64_t* off,
                               const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out17,
                               void* stream);
+int launch_attention_forest(const ForestView& fv, int forest, const int32_t* q, const int32_t* kv,
+                            const int64_t* off, const uint8_t* dec, int64_t nb, fs_attn_params prm,
+                            double* out, int n_sms, void* stream);
 int launch_route_uniform(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
                          int32_t* counts, int32_t* status, void* stream);
 int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int32_t* pidx,

@@ -1,0 +1,1682 @@
+// fs_sim.cuh -- batched discrete-event simulation of independent Frontier
+// instances: one warp per instance, state as struct-of-arrays in HBM.
+//
+// Reference behaviour restated here (pkg/src/frontier_sim/...):
+//   core.py:135-211           (timestamp, seq) event order, event budget
+//   orchestrator/base.py      kick / start_batch / complete_request / run
+//   orchestrator/colocated.py round-robin, prefill-first, continuous batching
+//   orchestrator/pd.py        least-outstanding prefill routing, FIFO KV transfer
+//                             queue with decode-memory backpressure
+//   orchestrator/af.py        AF step graph under 4 exclusive resources
+//   cluster.py                KvPool, admission (fcfs / fcfs_skip / priority),
+//                             OperatorCosts, execute_batch
+//   metrics.py:81-178         compute_metrics (separate kernel, fs_metrics.cu)
+//
+// Design (B200-first, not a translation of the reference's object graph):
+//  * Only state-changing events live in a per-instance binary heap (BATCH_START,
+//    BATCH_COMPLETE, KV_CACHE_TRANSFER_DONE); arrivals are a sorted cursor that
+//    wins timestamp ties (they hold seq 0..N-1, base.py:167-177). The no-op
+//    event kinds are counted, not stored -- skipping their sequence numbers
+//    preserves the relative order of every stored event.
+//  * A running request's completion step is known when it starts decoding, so
+//    a decode iteration is O(1): batch size and context sum are maintained
+//    incrementally and the running list is scanned only when the earliest
+//    finish step is reached.
+//  * Admission is a warp prefix-scan over the queue with a ballot for the
+//    first request that does not fit (fcfs / priority) or an iterative ballot
+//    (fcfs_skip).
+//  * The AF step graph (af.py:100-229) is list-scheduled in closed form per
+//    step; only its completion becomes an event.
+//  * MoE routing is warp-cooperative Philox (fs_route.cuh); per-layer router
+//    seeds (SHA-256 + two SeedSequence hashes) are derived one layer per lane.
+//
+// Per-warp scalar state is held redundantly in every lane's registers; global
+// scalar writes are issued by lane 0 and ordered with __syncwarp().
+#pragma once
+// Compiled twice (fs_engine.cu, fs_engine_learned.cu): FS_LEARNED selects the
+// learned attention model call sites, FS_SIM_NS the namespace of the variant.
+#include <cuda_runtime.h>
+
+#include "fs_device.cuh"
+#include "fs_engine.h"
+#include "fs_route.cuh"
+
+namespace fs {
+namespace FS_SIM_NS {
+
+enum { K_BATCH_START = 1, K_BATCH_COMPLETE = 2, K_KV_DONE = 3 };
+enum { PH_PREFILL = 0, PH_DECODE = 1, PH_AF = 2 };
+
+constexpr int kWarpsPerCta = 4;
+constexpr int kLayerChunk = 32;
+constexpr int kSlabBytes = 12 * 1024;  // per-warp shared-memory slab for hot instance state
+constexpr int32_t kNoFinish = 0x7fffffff;
+
+struct __align__(16) WarpSmem {
+  uint64_t keys[kLayerChunk][2];
+  int64_t af_attn[FS_MAX_MICRO_BATCHES];
+  int64_t af_xfer[FS_MAX_MICRO_BATCHES];
+  int32_t af_size[FS_MAX_MICRO_BATCHES];
+  int32_t af_stage[FS_MAX_MICRO_BATCHES];
+  int counts[FS_MAX_EXPERTS];
+#if FS_LEARNED
+  double fx[17];                   // learned attention model: feature vector
+  double fvals[kMaxForestTrees];   // ... and per-tree leaf values
+#endif
+};
+
+struct Inst {
+  const fs_instance_desc* d;
+  int idx, N, R, mode, lane, slot;
+  int64_t ro;      // request offset (global index of local request 0)
+  int rb;          // global index of local replica 0
+  int32_t* lists;  // 3*N ints per replica: queue, running, inflight members
+  HEv* heap;
+  RepState* rs;    // replica states (shared-memory slab or HBM)
+  int32_t* fin;    // per-request finish step, local index (slab or HBM)
+  int hn;
+  int64_t now, seq, events, max_events;
+  int rr, n_done, cursor;
+  int status, detail;
+  int xh, xt;  // PD transfer FIFO (ring of N slots at xfer + ro)
+  int64_t af_counter;
+  int64_t af_busy[4];
+  double bubble_weighted;
+  int64_t bubble_total;
+  int64_t prefill_batches, decode_batches, af_steps, moe_samples, routing_calls;
+  int32_t log_batches, log_moff, log_eoff, log_routes;
+};
+
+__device__ __forceinline__ int32_t* qlist(const Inst& I, int r) { return I.lists + (int64_t)r * 3 * I.N; }
+__device__ __forceinline__ int32_t* rlist(const Inst& I, int r) { return qlist(I, r) + I.N; }
+__device__ __forceinline__ int32_t* ilist(const Inst& I, int r) { return qlist(I, r) + 2 * I.N; }
+__device__ __forceinline__ int64_t gi(const Inst& I, int i) { return I.ro + i; }
+
+__device__ __forceinline__ void fail(Inst& I, int st, int detail) {
+  if (I.status == FS_OK) { I.status = st; I.detail = detail; }
+}
+
+// ---- replica state: every lane loads the same struct; lane 0 stores -------------
+__device__ __forceinline__ RepState load_rep(const EngineParams& P, const Inst& I, int r) {
+  __syncwarp();
+  return I.rs[r];
+}
+__device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, int r,
+                                          const RepState& s) {
+  __syncwarp();
+  if (I.lane == 0) I.rs[r] = s;
+  __syncwarp();
+}
+
+// ---- event heap (lane 0 mutates, the popped event is broadcast) ----------------
+__device__ __forceinline__ bool hev_less(const HEv& a, const HEv& b) {
+  return a.t < b.t || (a.t == b.t && a.seq < b.seq);
+}
+__device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
+  if (t < I.now) { fail(I, FS_ERR_SCHEDULING_IN_PAST, kind); return; }
+  __syncwarp();
+  if (I.lane == 0) {
+    HEv e;
+    e.t = t; e.seq = I.seq; e.kind = kind; e.a = a; e.b = b;
+    int i = I.hn;
+    while (i > 0) {
+      int p = (i - 1) >> 1;
+      HEv pe = I.heap[p];
+      if (!hev_less(e, pe)) break;
+      I.heap[i] = pe;
+      i = p;
+    }
+    I.heap[i] = e;
+  }
+  I.hn++;
+  I.seq++;
+  __syncwarp();
+}
+__device__ HEv heap_pop(Inst& I) {
+  HEv top;
+  top.t = 0; top.seq = 0; top.kind = 0; top.a = 0; top.b = 0;
+  __syncwarp();
+  if (I.lane == 0) {
+    top = I.heap[0];
+    const int n = I.hn - 1;
+    const HEv last = I.heap[n];
+    int i = 0;
+    for (;;) {
+      int l = 2 * i + 1, r = l + 1, m = -1;
+      HEv cur = last;
+      if (l < n) { HEv le = I.heap[l]; if (hev_less(le, cur)) { m = l; cur = le; } }
+      if (r < n) { HEv re = I.heap[r]; if (hev_less(re, cur)) { m = r; cur = re; } }
+      if (m < 0) break;
+      I.heap[i] = cur;
+      i = m;
+    }
+    if (n > 0) I.heap[i] = last;
+  }
+  I.hn--;
+  __syncwarp();
+  top.t = __shfl_sync(FS_FULL, top.t, 0);
+  top.kind = __shfl_sync(FS_FULL, top.kind, 0);
+  top.a = __shfl_sync(FS_FULL, top.a, 0);
+  top.b = __shfl_sync(FS_FULL, top.b, 0);
+  return top;
+}
+__device__ __forceinline__ int64_t heap_top_t(const Inst& I) {
+  int64_t t = 0;
+  if (I.lane == 0) t = I.heap[0].t;
+  return __shfl_sync(FS_FULL, t, 0);
+}
+
+// ---- KvPool (cluster.py:36-93): every reservation here is a request's first in
+// its pool, so the charge is rounded(tokens) and release returns the same ----------
+__device__ __forceinline__ int64_t pool_rounded(const fs_instance_desc* d, int64_t tokens) {
+  if (!d->paged) return tokens;
+  const int64_t b = d->block_tokens;
+  return (tokens + b - 1) / b * b;
+}
+
+// ---- OperatorCosts (cluster.py:252-314) ----------------------------------------------
+__device__ __forceinline__ void heads_of(const fs_instance_desc* d, int tp, int& hq, int& hkv) {
+  hq = d->num_query_heads / tp; if (hq < 1) hq = 1;
+  hkv = d->num_kv_heads / tp; if (hkv < 1) hkv = 1;
+}
+__device__ __forceinline__ double qkv_us(const fs_instance_desc* d, const fs_cost_ctx& c, int64_t n) {
+  int hq, hkv;
+  heads_of(d, c.tp, hq, hkv);
+  return linear_us(n, (int64_t)(hq + 2 * hkv) * d->head_dim, d->d_model, c, d->dtype_bytes);
+}
+__device__ __forceinline__ double out_us(const fs_instance_desc* d, const fs_cost_ctx& c, int64_t n) {
+  int hq, hkv;
+  heads_of(d, c.tp, hq, hkv);
+  return linear_us(n, d->d_model, (int64_t)hq * d->head_dim, c, d->dtype_bytes);
+}
+__device__ __forceinline__ double tpcoll_us(const fs_instance_desc* d, const fs_cost_ctx& c, int64_t n) {
+  const int64_t b = n * (int64_t)d->d_model * d->dtype_bytes;
+  return collective_int(true, b, c.tp, d->intra_latency_s, d->intra_bandwidth_bps) * 1e6;
+}
+__device__ __forceinline__ double dense_ffn_us(const fs_instance_desc* d, const fs_cost_ctx& c, int64_t n) {
+  int64_t dff = d->d_ff / c.tp;
+  if (dff < 1) dff = 1;
+  return grouped_gemm_us(n, 1, d->d_model, dff, d->ffn_matrices, c, d->dtype_bytes);
+}
+__device__ __forceinline__ double attn_cost_us(const fs_instance_desc* d, const fs_cost_ctx& c,
+                                               double flops, int64_t sum_q, int64_t sum_kv) {
+  int hq, hkv;
+  heads_of(d, c.tp, hq, hkv);
+  return attention_us_from(flops, sum_q, sum_kv, hq, hkv, d->head_dim, c, d->dtype_bytes);
+}
+
+// ---- router seeds for 32 layers at a time, one layer per lane --------------------------
+__device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int prefix, int mb,
+                                  int64_t step, int l0, int L, WarpSmem* sm) {
+  __syncwarp();
+  const int layer = l0 + I.lane;
+  if (layer < L) {
+    const fs_seed_prefix* pf = &P.prefixes[prefix];
+    int64_t ints[3];
+    int n = 0;
+    if (mb > 0) ints[n++] = mb;
+    ints[n++] = step;
+    ints[n++] = layer;
+    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->len / 64,
+                                                 pf->bytes, pf->len, ints, n);
+    uint64_t key[2];
+    routing_key((uint64_t)seed, key);
+    sm->keys[I.lane][0] = key[0];
+    sm->keys[I.lane][1] = key[1];
+  }
+  __syncwarp();
+}
+
+// ---- one router call (routing.py:65-113) ------------------------------------------------
+__device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
+                           uint64_t k0, uint64_t k1, WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  const int E = d->num_experts, k = d->top_k;
+  if (!(1 <= k && k <= E)) return FS_ERR_INVALID_TOPK;
+  if (E > FS_MAX_EXPERTS) return FS_ERR_CAPACITY;
+  if (T < 0) return FS_ERR_ROUTING;
+  if (policy == FS_ROUTE_TRACE) {
+    if (d->n_trace_counts != E) return FS_ERR_ROUTING;
+    int64_t s = 0;
+    int neg = 0;
+    __syncwarp();
+    for (int e = I.lane; e < E; e += 32) {
+      const int64_t c = P.trace_counts[d->trace_offset + e];
+      neg |= c < 0;
+      s += c;
+      sm->counts[e] = (int)c;
+    }
+    __syncwarp();
+    s = warp_sum_i64(s);
+    neg = __any_sync(FS_FULL, neg);
+    if (neg || s != T * k) return FS_ERR_ROUTING;
+    return FS_OK;
+  }
+  if (T == 0 || k == E || policy == FS_ROUTE_UNIFORM) {
+    if (T > 0 && k < E && k > FS_MAX_TOPK) return FS_ERR_CAPACITY;
+    __syncwarp();
+    return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
+  }
+  return FS_ERR_UNSUPPORTED;  // dirichlet_skew is not on the device path yet
+}
+
+__device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
+                          int64_t T, const WarpSmem* sm) {
+  if (!P.log_enabled || !P.log.routes) return;
+  const int E = I.d->num_experts;
+  const int32_t c = I.log_routes;
+  const int64_t cb = (int64_t)c * E;
+  if (c < P.log.route_cap && cb + E <= P.log.counts_cap) {
+    if (I.lane == 0) {
+      fs_route_rec rec;
+      rec.replica = r; rec.micro_batch = mb; rec.step = step; rec.layer = layer;
+      rec.tokens = (int32_t)T; rec.counts_offset = (int32_t)cb; rec.n_experts = E;
+      P.log.routes[P.log.route_base[I.idx] + c] = rec;
+    }
+    for (int e = I.lane; e < E; e += 32) P.log.counts[P.log.counts_base[I.idx] + cb + e] = sm->counts[e];
+    I.log_routes = c + 1;
+  } else if (I.lane == 0) {
+    P.log.truncated[I.idx] = 1;
+  }
+  __syncwarp();
+}
+
+// ---- routing job board -----------------------------------------------------------------------
+// One batch's uniform router calls (up to kJobLayers layers x T tokens x E
+// experts of Philox draws) dwarf everything else an MoE instance does, and a
+// sweep's MoE instances are its longest. So the owning warp publishes the
+// calls as a job of row chunks on a GPU-wide board; it works on its own job,
+// and every warp whose share of the instance queue is exhausted scans the
+// board and claims chunks of other warps' jobs. A claimed chunk pins its job
+// (the job cannot complete, hence cannot be replaced, until the chunk's
+// completion is counted), so chunk parameters are stable for the claimant.
+// Counts land in the job's global tally with warp-aggregated atomics; the owner
+// waits for every chunk, fences, and reads the tally through L2.
+constexpr unsigned kChunkBits = 20;
+constexpr unsigned long long kChunkMask = (1ull << kChunkBits) - 1;
+constexpr int kMaxChunks = 1 << 18;
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
+  return *reinterpret_cast<const volatile int32_t*>(p);
+}
+
+// returns a claimed chunk index or -1 (same on all lanes). A successful claim is
+// followed by a fence so the job parameters, written before the job was
+// published, are visible; the claimant of the last chunk closes the job.
+__device__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
+  long long c = -1;
+  if (lane == 0) {
+    const unsigned long long v = ld_volatile_u64(&job->ctr);
+    if ((v & kChunkMask) < ((v >> kChunkBits) & kChunkMask)) {
+      const unsigned long long old = atomicAdd(&job->ctr, 1ull);
+      const unsigned long long n = (old >> kChunkBits) & kChunkMask;
+      if ((old & kChunkMask) < n) {
+        c = (long long)(old & kChunkMask);
+        if ((unsigned long long)c + 1 == n) atomicSub(P.open_jobs, 1);
+      }
+    }
+  }
+  c = __shfl_sync(FS_FULL, c, 0);
+  if (c >= 0) __threadfence();
+  return (int)c;
+}
+
+// One pass: lane (row r of `layer`, segment seg) keeps the kc smallest keys of
+// its draws. Fast path: 32-bit surrogate keys (the top 32 bits of each draw,
+// whose order agrees with the 53-bit key except on a tie of those bits) with
+// the expert index in the low `eb` bits; the set is exact unless the k-th and
+// (k+1)-th surrogates tie above the index bits, in which case the pass is
+// redone with the exact 64-bit keys (which also detects a true tie).
+template <int KCAP>
+__device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool active, uint64_t rb,
+                                          int e0, int e1, uint32_t emask, uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) top[j] = 0xFFFFFFFFu;
+  uint32_t thr = 0xFFFFFFFFu;
+  if (!active || e0 >= e1) return;
+  const uint64_t n0 = rb + e0, n1 = rb + e1;
+  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) {
+    const U4 blk = philox4x64_10(b + 1, k0, k1);
+    const uint64_t base = 4 * b;
+    const int jlo = n0 > base ? (int)(n0 - base) : 0;
+    const int jhi = (n1 - base) < 4 ? (int)(n1 - base) : 4;
+    const uint32_t eb0 = (uint32_t)(base - rb);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (j >= jlo && j < jhi) {
+        uint32_t x = ((uint32_t)(blk.v[j] >> 32) & ~emask) | (eb0 + (uint32_t)j);
+        if (KCAP <= 4 || x < thr) {
+#pragma unroll
+          for (int q = 0; q < KCAP; q++) {
+            const uint32_t lo = min(top[q], x);
+            x = max(top[q], x);
+            top[q] = lo;
+          }
+          if (KCAP > 4) {
+#pragma unroll
+            for (int q = 0; q < KCAP; q++)
+              if (q == kc - 1) thr = top[q];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int KCAP>
+__device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+                                int lane) {
+  const int64_t T = __ldcg(&job->T);
+  const int E = __ldcg(&job->E), k = __ldcg(&job->k), nl = __ldcg(&job->nl);
+  const int nseg = __ldcg(&job->nseg), ppc = __ldcg(&job->passes_per_chunk);
+  const int rpp = 32 / nseg;
+  const int seg_len = (E + nseg - 1) / nseg;
+  const int64_t total_rows = (int64_t)nl * T;
+  const int kc = k + 1;
+  const int seg = lane & (nseg - 1);
+  const int e0 = seg * seg_len, e1 = min(E, e0 + seg_len);
+  int eb = 0;
+  while ((1 << eb) < E) eb++;
+  const uint32_t emask = (1u << eb) - 1u;
+  int tie = 0;
+  // this lane's first row; later passes advance it incrementally (no division)
+  const int64_t row0 = (int64_t)c * ppc * rpp;
+  int64_t row_j = row0 + lane / nseg;
+  int layer = (int)(row_j / T);
+  int64_t r = row_j - (int64_t)layer * T;
+  int key_layer = -1;
+  uint64_t k0 = 0, k1 = 0;
+  for (int p = 0; p < ppc; p++) {
+    if (row0 + (int64_t)p * rpp >= total_rows) break;
+    const bool active = row_j < total_rows;
+    if (active && layer != key_layer) {
+      k0 = __ldcg(&job->keys[layer][0]);
+      k1 = __ldcg(&job->keys[layer][1]);
+      key_layer = layer;
+    }
+    const uint64_t rb = (uint64_t)r * (uint64_t)E;
+    uint32_t top[KCAP];
+    pass_fast<KCAP>(top, kc, active, rb, e0, e1, emask, k0, k1);
+    for (int s = 1; s < nseg; s <<= 1) {
+      uint32_t other[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, top[j], s);
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) {
+        uint32_t x = other[j];
+#pragma unroll
+        for (int q = 0; q < KCAP; q++) {
+          const uint32_t lo = min(top[q], x);
+          x = max(top[q], x);
+          top[q] = lo;
+        }
+      }
+    }
+    const bool leader = active && seg == 0;
+    bool unsure = false;
+#pragma unroll
+    for (int j = 1; j < KCAP; j++)
+      if (j == k && leader && (top[j] >> eb) == (top[j - 1] >> eb)) unsure = true;
+    int ids[KCAP];
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) ids[j] = (int)(top[j] & emask);
+    if (__any_sync(FS_FULL, unsure)) {
+      // exact 64-bit redo of this pass
+      uint64_t t64[KCAP];
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
+      uint64_t thr = ~0ull;
+      if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+      for (int s = 1; s < nseg; s <<= 1) {
+        uint64_t other[KCAP];
+#pragma unroll
+        for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
+#pragma unroll
+        for (int j = 0; j < KCAP; j++)
+          if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
+      }
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) {
+        ids[j] = (int)(t64[j] & 0x7FF);
+        if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) {
+      if (j < k) {
+        const int key = leader ? layer * E + ids[j] : -1;
+        const unsigned grp = __match_any_sync(FS_FULL, key);
+        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counts[key], __popc(grp));
+      }
+    }
+    r += rpp;
+    row_j += rpp;
+    while (r >= T) { r -= T; layer++; }
+  }
+  if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
+}
+
+__device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+                              int lane) {
+  const int k = __ldcg(&job->k);
+  if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane);
+  else if (k + 1 <= 9) process_chunk_k<9>(P, job, counts, c, lane);
+  else process_chunk_k<FS_MAX_TOPK + 1>(P, job, counts, c, lane);
+  __threadfence();
+  if (lane == 0) atomicAdd(&job->done, 1);
+  __syncwarp();
+}
+
+__device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slot) {
+  return P.job_counts + (int64_t)slot * kJobLayers * P.job_max_e;
+}
+
+// Route layers [l0, l0+nl) of one batch; the tally of layer l0+j ends up at
+// job_counts_of(slot)[j*E ...]. Returns FS_OK or FS_ERR_ROUTING_TIE.
+__device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
+                             int l0, int nl, int64_t T) {
+  const fs_instance_desc* d = I.d;
+  RouteJob* job = &P.jobs[I.slot];
+  int32_t* counts = job_counts_of(P, I.slot);
+  const int E = d->num_experts, k = d->top_k;
+  // router seeds + Philox keys, one layer per lane (base.py:63-65, routing.py:59-62)
+  const int layer = l0 + I.lane;
+  if (I.lane < nl) {
+    const fs_seed_prefix* pf = &P.prefixes[prefix];
+    int64_t ints[3];
+    int n = 0;
+    if (mb > 0) ints[n++] = mb;
+    ints[n++] = step;
+    ints[n++] = layer;
+    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->len / 64,
+                                                 pf->bytes, pf->len, ints, n);
+    uint64_t key[2];
+    routing_key((uint64_t)seed, key);
+    job->keys[I.lane][0] = key[0];
+    job->keys[I.lane][1] = key[1];
+  }
+  for (int i = I.lane; i < nl * E; i += 32) counts[i] = 0;
+  // geometry: split rows into segments while there are few of them; a chunk
+  // carries >= ~16 Philox blocks per lane so claims and fences stay cheap
+  const int64_t rows = (int64_t)nl * T;
+  int nseg = 1;
+  while (nseg < 32 && (nseg * 2) * 4 <= E && rows * nseg < 2048) nseg *= 2;
+  const int rpp = 32 / nseg;
+  const int64_t passes = (rows + rpp - 1) / rpp;
+  const int blocks_per_pass = ((E + nseg - 1) / nseg + 3) / 4 + 1;
+  int ppc = 16 / blocks_per_pass;
+  if (ppc < 1) ppc = 1;
+  int64_t n_chunks = (passes + ppc - 1) / ppc;
+  if (n_chunks > kMaxChunks) {
+    ppc = (int)((passes + kMaxChunks - 1) / kMaxChunks);
+    n_chunks = (passes + ppc - 1) / ppc;
+  }
+  if (I.lane == 0) {
+    job->T = T; job->E = E; job->k = k; job->nl = nl; job->nseg = nseg;
+    job->passes_per_chunk = ppc; job->done = 0; job->tie = 0;
+  }
+  __syncwarp();
+  __threadfence();
+  const bool shared = n_chunks >= 4;  // small jobs are not worth publishing
+  if (I.lane == 0) {
+    const unsigned long long epoch =
+        ((ld_volatile_u64(&job->ctr) >> (2 * kChunkBits)) + 1) & 0xFFFFFFull;
+    const unsigned long long v = (epoch << (2 * kChunkBits)) |
+                                 ((unsigned long long)n_chunks << kChunkBits);
+    // a private job is published fully claimed, so helpers never see it
+    atomicExch(&job->ctr, shared ? v : (v | (unsigned long long)n_chunks));
+    if (shared) atomicAdd(P.open_jobs, 1);
+  }
+  __syncwarp();
+  if (shared) {
+    for (int c; (c = claim_chunk(P, job, I.lane)) >= 0;) process_chunk(P, job, counts, c, I.lane);
+    while (ld_volatile_i32(&job->done) < n_chunks) __nanosleep(64);
+  } else {
+    for (int c = 0; c < n_chunks; c++) process_chunk(P, job, counts, c, I.lane);
+  }
+  __threadfence();
+  __syncwarp();
+  return ld_volatile_i32(&job->tie) ? FS_ERR_ROUTING_TIE : FS_OK;
+}
+
+// uniform routing with real draws goes through the job board; the trace policy
+// and the RNG-free shortcuts (T == 0, top_k == E) stay on the owning warp
+__device__ __forceinline__ bool use_job_board(const fs_instance_desc* d, int policy, int64_t T) {
+  return policy == FS_ROUTE_UNIFORM && T > 0 && d->top_k < d->num_experts &&
+         d->top_k >= 1 && d->top_k <= FS_MAX_TOPK && d->num_experts <= FS_MAX_EXPERTS;
+}
+
+// copy one layer's tally from the job (through L2) to the warp's counts
+__device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, WarpSmem* sm) {
+  const int E = I.d->num_experts;
+  const int32_t* counts = job_counts_of(P, I.slot) + (int64_t)j * E;
+  __syncwarp();
+  for (int e = I.lane; e < E; e += 32) sm->counts[e] = __ldcg(counts + e);
+  __syncwarp();
+}
+
+// warps with no instance left help route other warps' jobs until every
+// instance has finished; they sleep (exponential backoff) while no job is open
+__device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
+  const int ns = P.n_slots;
+  const int start = (int)(((unsigned)my_slot * 37u) % (unsigned)ns);
+  unsigned backoff = 32;
+  while (ld_volatile_i32(P.inst_done) < P.n_inst) {
+    if (ld_volatile_i32(P.open_jobs) <= 0) {
+      __nanosleep(backoff);
+      backoff = backoff < 4096 ? backoff * 2 : 4096;
+      continue;
+    }
+    backoff = 32;
+    for (int base = 0; base < ns; base += 32) {
+      int s = start + base + lane;
+      if (s >= ns) s -= ns;
+      bool avail = false;
+      if (base + lane < ns) {
+        const unsigned long long v = ld_volatile_u64(&P.jobs[s].ctr);
+        avail = (v & kChunkMask) < ((v >> kChunkBits) & kChunkMask);
+      }
+      unsigned m = __ballot_sync(FS_FULL, avail);
+      while (m) {
+        const int pick = __ffs(m) - 1;
+        m &= m - 1;
+        const int sp = __shfl_sync(FS_FULL, s, pick);
+        RouteJob* job = &P.jobs[sp];
+        for (int c; (c = claim_chunk(P, job, lane)) >= 0;)
+          process_chunk(P, job, job_counts_of(P, sp), c, lane);
+      }
+    }
+  }
+}
+
+// ---- execute_batch (cluster.py:317-346) ---------------------------------------------------
+struct BatchShape {
+  int64_t n_tokens, sum_q, sum_kv;
+  double attn_flops;
+#if FS_LEARNED
+  double learned_attn;  // learned-model attention us, NaN = analytic
+#endif
+};
+
+#if FS_LEARNED
+// CostModel.predict_attention with a learned model (model.py:313-321): the
+// attention_v1 features of the batch members (prefill: q = kv = prompt;
+// decode: q = 1, kv = prompt + emitted), then the forest. Out of line: only
+// the learned simulation variant has these call sites.
+__device__ __noinline__ double learned_attention_us(const EngineParams& P, Inst& I,
+                                                    bool decode, const int32_t* members, int n,
+                                                    int dstep, int tp, WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  if (d->attn_forest < 0) {  // wrong schema for the attention slot (model.py:315-320)
+    fail(I, FS_ERR_SCHEMA, 0);
+    return 0.0;
+  }
+  int hq, hkv;
+  heads_of(d, tp, hq, hkv);
+  auto fq = [&](int64_t i) -> int64_t {
+    return decode ? 1 : (int64_t)P.prompt[gi(I, members[i])];
+  };
+  auto fk = [&](int64_t i) -> int64_t {
+    const int req = members[i];
+    if (!decode) return P.prompt[gi(I, req)];
+    return (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)] + dstep - I.fin[req];
+  };
+  double x[17];
+  attention_features_w(decode, n, fq, fk, hq, hkv, d->head_dim, I.lane, x);
+  __syncwarp();
+  if (I.lane < 17) {
+#pragma unroll
+    for (int j = 0; j < 17; j++)
+      if (j == I.lane) sm->fx[j] = x[j];
+  }
+  __syncwarp();
+  const double v = forest_predict_w(P.fv, d->attn_forest, sm->fx, sm->fvals, I.lane);
+  __syncwarp();
+  return v;
+}
+
+// Dense FFN with a learned grouped-GEMM model (cluster.py:286-296): one local
+// expert holding all n tokens, so GroupedGemmFeatures.vector() is closed form
+// (features.py:166-209: ratio 1, max/mean 1, cv 0, entropy 1, std 0).
+__device__ __noinline__ double learned_dense_ffn_us(const EngineParams& P, Inst& I,
+                                                    const fs_cost_ctx& c, int64_t n, WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  if (d->gg_forest < 0) {  // check_schema("grouped_gemm_v1") (model.py:325)
+    fail(I, FS_ERR_SCHEMA, 0);
+    return 0.0;
+  }
+  if (n < 1) {
+    fail(I, FS_ERR_EMPTY_BATCH, 2);
+    return 0.0;
+  }
+  int64_t dff = d->d_ff / c.tp;
+  if (dff < 1) dff = 1;
+  __syncwarp();
+  if (I.lane == 0) {
+    double* x = sm->fx;
+    x[0] = (double)n; x[1] = 1.0; x[2] = (double)d->d_model; x[3] = (double)dff;
+    x[4] = 1.0; x[5] = 1.0; x[6] = 1.0; x[7] = 0.0; x[8] = 1.0;
+    x[9] = (double)n; x[10] = (double)n; x[11] = 0.0;
+  }
+  __syncwarp();
+  const double v = forest_predict_w(P.fv, d->gg_forest, sm->fx, sm->fvals, I.lane);
+  __syncwarp();
+  return v;
+}
+#define FFN_DENSE_US(c, n) \
+  (d->gg_forest != -1 ? learned_dense_ffn_us(P, I, (c), (n), sm) : dense_ffn_us(d, (c), (n)))
+#else
+#define FFN_DENSE_US(c, n) dense_ffn_us(d, (c), (n))
+#endif
+
+// Duration in us (same on all lanes). moe_out (global) receives per-layer raw
+// moe_imbalance ratios when non-null.
+__device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
+                                const BatchShape& b, int64_t step, WarpSmem* sm,
+                                double* moe_out) {
+  const fs_instance_desc* d = I.d;
+  const fs_cost_ctx c = rd.cost;
+  const int L = d->num_layers;
+  const int64_t n = b.n_tokens;
+  const double qkv = qkv_us(d, c, n);
+#if FS_LEARNED
+  const double att = isnan(b.learned_attn) ? attn_cost_us(d, c, b.attn_flops, b.sum_q, b.sum_kv)
+                                           : b.learned_attn;
+#else
+  const double att = attn_cost_us(d, c, b.attn_flops, b.sum_q, b.sum_kv);
+#endif
+  const double out = out_us(d, c, n);
+  const double coll = tpcoll_us(d, c, n);
+  PySum ls;
+  ls.init();
+  if (!d->has_moe) {
+    const double ffn = FFN_DENSE_US(c, n);
+    double tot = qkv + att;
+    tot = tot + out;
+    tot = tot + coll;
+    tot = tot + ffn;
+    tot = tot + coll;
+    for (int l = 0; l < L; l++) ls.add(tot);  // never L * tot: Python adds layer by layer
+  } else {
+    const bool board = use_job_board(I.d, d->routing_policy, n);
+    const bool log_routes = P.log_enabled && P.log.routes;
+    for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
+      const int lend = min(L, l0 + kLayerChunk);
+      double lane_ffn = 0.0, lane_ratio = 1.0;
+      if (board) {
+        int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n);
+        if (st == FS_OK)
+          st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, n, d->num_experts,
+                                d->top_k, d->d_model, d->expert_d_ff, d->ffn_matrices,
+                                d->dtype_bytes, c.ep, c.moe_tp, d->intra_latency_s,
+                                d->intra_bandwidth_bps, c, &lane_ffn,
+                                moe_out ? &lane_ratio : nullptr);
+        if (st != FS_OK) { fail(I, st, l0); return 0.0; }
+      } else {
+        derive_layer_keys(P, I, rd.prefix, 0, step, l0, L, sm);
+      }
+      for (int l = l0; l < lend; l++) {
+        double ffn, ratio = 1.0;
+        if (board) {
+          ffn = __shfl_sync(FS_FULL, lane_ffn, l - l0);
+          ratio = __shfl_sync(FS_FULL, lane_ratio, l - l0);
+          I.routing_calls++;
+          if (log_routes) {
+            load_job_layer(P, I, l - l0, sm);
+            log_route(P, I, r, 0, step, l, n, sm);
+          }
+        } else {
+          int st = route_layer(P, I, d->routing_policy, n, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
+          if (st != FS_OK) { fail(I, st, l); return 0.0; }
+          I.routing_calls++;
+          log_route(P, I, r, 0, step, l, n, sm);
+          st = moe_layer_warp(I.lane, sm->counts, n, d->num_experts, d->top_k, d->d_model,
+                              d->expert_d_ff, d->ffn_matrices, d->dtype_bytes, c.ep, c.moe_tp,
+                              d->intra_latency_s, d->intra_bandwidth_bps, c, &ffn,
+                              moe_out ? &ratio : nullptr);
+          if (st != FS_OK) { fail(I, st, l); return 0.0; }
+        }
+        __syncwarp();
+        if (moe_out && I.lane == 0) moe_out[l] = ratio;
+        double tot = qkv + att;
+        tot = tot + out;
+        tot = tot + coll;
+        tot = tot + ffn;
+        tot = tot + coll;
+        ls.add(tot);
+      }
+    }
+  }
+  const int64_t bytes = n * (int64_t)d->d_model * d->dtype_bytes;
+  const double tt = d->intra_latency_s + i2d(bytes) / d->intra_bandwidth_bps;
+  const double pp = (double)(c.pp - 1) * (tt * 1e6);
+  return ls.result() + pp;
+}
+
+// ---- optional batch log -------------------------------------------------------------------
+// A batch's moe-ratio slot is reserved when it starts: several replicas can have
+// batches in flight, so slots are handed out in start order and each batch
+// record points at its own. Returns offset + 1 (0 = not logged).
+__device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
+  if (!P.log_enabled || !P.log.batches || !I.d->has_moe) return 0;
+  if (I.log_eoff + I.d->num_layers > P.log.moe_cap) return 0;
+  const int32_t off = I.log_eoff;
+  I.log_eoff += I.d->num_layers;
+  return off + 1;
+}
+__device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
+                          const int32_t* members, int nm, int32_t moe_off1) {
+  if (!P.log_enabled || !P.log.batches) return;
+  const int n_moe = moe_off1 ? I.d->num_layers : 0;
+  const bool need_moe = I.d->has_moe && phase != PH_AF;
+  const int32_t c = I.log_batches;
+  if (c < P.log.batch_cap && I.log_moff + nm <= P.log.member_cap && (!need_moe || moe_off1)) {
+    if (I.lane == 0) {
+      fs_batch_rec rec;
+      rec.replica = r; rec.phase = phase; rec.t_complete = I.now; rec.duration_ns = dur;
+      rec.n_members = nm; rec.member_offset = I.log_moff;
+      rec.moe_offset = n_moe ? moe_off1 - 1 : -1;
+      rec.n_moe = n_moe;
+      P.log.batches[P.log.batch_base[I.idx] + c] = rec;
+    }
+    const int64_t mb = P.log.member_base[I.idx] + I.log_moff;
+    for (int i = I.lane; i < nm; i += 32) P.log.members[mb + i] = members[i];
+    I.log_moff += nm;
+    I.log_batches = c + 1;
+  } else if (I.lane == 0) {
+    P.log.truncated[I.idx] = 1;
+  }
+  __syncwarp();
+}
+
+// ---- list helpers ---------------------------------------------------------------------------
+// remove the first m entries (stable shift)
+__device__ void list_drop_front(int32_t* a, int len, int m, int lane) {
+  if (m == 0) return;
+  for (int base = 0; base < len - m; base += 32) {
+    const int i = base + lane;
+    const int v = (i < len - m) ? a[i + m] : 0;
+    __syncwarp();
+    if (i < len - m) a[i] = v;
+    __syncwarp();
+  }
+}
+// insert v at position pos (shifting the tail right)
+__device__ void list_insert(int32_t* a, int len, int pos, int v, int lane) {
+  for (int top = len; top > pos; top -= 32) {
+    const int i = top - 1 - lane;  // source index, descending
+    const bool act = i >= pos;
+    const int x = act ? a[i] : 0;
+    __syncwarp();
+    if (act) a[i + 1] = x;
+    __syncwarp();
+  }
+  if (lane == 0) a[pos] = v;
+  __syncwarp();
+}
+
+// priority key (cluster.py:153-157): (prompt, arrival, id) or (arrival, id)
+__device__ __forceinline__ bool prio_less(const EngineParams& P, const Inst& I, int a, int b) {
+  if (I.d->priority_key == FS_PRIO_PROMPT) {
+    const int pa = P.prompt[gi(I, a)], pb = P.prompt[gi(I, b)];
+    if (pa != pb) return pa < pb;
+  }
+  const int64_t ta = P.arrival[gi(I, a)], tb = P.arrival[gi(I, b)];
+  if (ta != tb) return ta < tb;
+  return P.id_rank[gi(I, a)] < P.id_rank[gi(I, b)];
+}
+
+// enqueue a waiting request; priority admission keeps the queue in key order
+__device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
+  int32_t* q = qlist(I, r);
+  if (I.d->admission == FS_ADMIT_PRIORITY) {
+    int pos = 0;
+    for (int base = 0; base < s.qlen; base += 32) {
+      const int i = base + I.lane;
+      const bool less = i < s.qlen && prio_less(P, I, q[i], req);
+      pos += __popc(__ballot_sync(FS_FULL, less));
+    }
+    list_insert(q, s.qlen, pos, req, I.lane);
+  } else {
+    __syncwarp();
+    if (I.lane == 0) q[s.qlen] = req;
+    __syncwarp();
+  }
+  s.qlen++;
+}
+
+// FIFO head of a queue (the queue in priority mode is key-ordered; the FIFO
+// head is the earliest-arrived request, i.e. the smallest local index)
+__device__ int queue_head(const Inst& I, int r, const RepState& s) {
+  const int32_t* q = qlist(I, r);
+  if (I.d->admission != FS_ADMIT_PRIORITY) return q[0];
+  int64_t m = 0x7fffffff;
+  for (int i = I.lane; i < s.qlen; i += 32) m = min(m, (int64_t)q[i]);
+  return (int)warp_min_i64(m);
+}
+
+// ---- build_prefill_batch (cluster.py:145-183) ------------------------------------------------
+struct Admit {
+  int m;
+  int64_t sum_p, sum_p2, max_p, charge;
+};
+
+// Admitted members (candidate order) go to the inflight list and leave the queue.
+__device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
+                               int running_count, int64_t capacity) {
+  const fs_instance_desc* d = I.d;
+  int32_t* q = qlist(I, r);
+  int32_t* il = ilist(I, r);
+  const int64_t seats = (int64_t)d->max_num_seqs - running_count;
+  const int64_t mbt = d->max_batch_tokens;
+  const int64_t headroom = capacity - s.used;
+  const unsigned lt = (1u << I.lane) - 1u;
+  Admit A;
+  A.m = 0; A.sum_p = 0; A.sum_p2 = 0; A.max_p = 0; A.charge = 0;
+  int64_t tokens = 0;
+  __syncwarp();
+  if (d->admission != FS_ADMIT_FCFS_SKIP) {
+    // strict order: the admitted set is the longest fitting prefix
+    for (int base = 0; base < s.qlen; base += 32) {
+      const int i = base + I.lane;
+      const bool valid = i < s.qlen;
+      const int req = valid ? q[i] : 0;
+      const int64_t p = valid ? P.prompt[gi(I, req)] : 0;
+      const int64_t fp = valid ? pool_rounded(d, full ? p + P.output[gi(I, req)] : p) : 0;
+      const int64_t cp = warp_incl_scan_i64(p, I.lane);
+      const int64_t cf = warp_incl_scan_i64(fp, I.lane);
+      const bool ok = valid && (A.m + I.lane < seats) && (tokens + cp <= mbt) &&
+                      (A.charge + cf <= headroom);
+      const unsigned vm = __ballot_sync(FS_FULL, valid);
+      const unsigned bad = vm & ~__ballot_sync(FS_FULL, ok);
+      const int nadm = bad ? __ffs(bad) - 1 : __popc(vm);
+      const bool adm = I.lane < nadm;
+      if (adm) il[A.m + I.lane] = req;
+      const int64_t ap = adm ? p : 0;
+      A.sum_p += warp_sum_i64(ap);
+      A.sum_p2 += warp_sum_i64(ap * ap);
+      A.max_p = max(A.max_p, warp_max_i64(ap));
+      A.charge += warp_sum_i64(adm ? fp : 0);
+      tokens = A.sum_p;
+      A.m += nadm;
+      if (bad) break;
+    }
+    __syncwarp();
+    list_drop_front(q, s.qlen, A.m, I.lane);
+    s.qlen -= A.m;
+  } else {
+    // fcfs_skip: greedy in queue order; a request that does not fit is skipped
+    // (totals only grow, so it can never fit later in the same scan)
+    int w = 0;
+    for (int base = 0; base < s.qlen; base += 32) {
+      const int i = base + I.lane;
+      const bool valid = i < s.qlen;
+      const int req = valid ? q[i] : 0;
+      const int64_t p = valid ? P.prompt[gi(I, req)] : 0;
+      const int64_t fp = valid ? pool_rounded(d, full ? p + P.output[gi(I, req)] : p) : 0;
+      unsigned admitted = 0;
+      int last = -1;
+      for (;;) {
+        const bool fits = valid && I.lane > last && (A.m < seats) && (tokens + p <= mbt) &&
+                          (A.charge + fp <= headroom);
+        const unsigned fm = __ballot_sync(FS_FULL, fits);
+        if (!fm) break;
+        const int f = __ffs(fm) - 1;
+        admitted |= 1u << f;
+        const int64_t pv = __shfl_sync(FS_FULL, p, f);
+        const int64_t fpv = __shfl_sync(FS_FULL, fp, f);
+        if (I.lane == f) il[A.m] = req;
+        A.m++;
+        tokens += pv;
+        A.charge += fpv;
+        A.sum_p += pv;
+        A.sum_p2 += pv * pv;
+        A.max_p = max(A.max_p, pv);
+        last = f;
+      }
+      const unsigned keep = __ballot_sync(FS_FULL, valid) & ~admitted;
+      __syncwarp();
+      if (keep & (1u << I.lane)) q[w + __popc(keep & lt)] = req;
+      w += __popc(keep);
+      __syncwarp();
+    }
+    s.qlen = w;
+  }
+  __syncwarp();
+  return A;
+}
+
+// ---- batch launch helpers ----------------------------------------------------------------------
+__device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
+                             const fs_replica_desc& rd, const BatchShape& b, int phase,
+                             WarpSmem* sm) {
+  const int32_t moe_off1 = log_moe_reserve(P, I);
+  double* moe_slot = moe_off1 ? P.log.moe_ratio + P.log.moe_base[I.idx] + (moe_off1 - 1) : nullptr;
+  const double us = execute_batch(P, I, r, rd, b, s.steps, sm, moe_slot);
+  if (I.status) return;
+  const int64_t dur = py_round(us * 1000.0);
+  s.busy = 1;
+  s.steps++;
+  s.inflight_phase = phase;
+  s.inflight_dur = dur;
+  s.inflight_moe = moe_off1;
+  heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
+}
+
+__device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
+                              const fs_replica_desc& rd, const Admit& A, WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  BatchShape b;
+  b.n_tokens = A.sum_p;
+  b.sum_q = A.sum_p;
+  b.sum_kv = A.sum_p;
+  int hq, hkv;
+  heads_of(d, rd.cost.tp, hq, hkv);
+  const int64_t hd = (int64_t)hq * d->head_dim;
+  // Each member contributes the exact integer 2*l*l*hd (c == l); while every
+  // term and partial sum stays below 2^53 the sequential fp64 sum is exact in
+  // any order, so the integer sum is bit-identical.
+  const double lim = 9007199254740992.0;
+  if (4.0 * (double)A.max_p * (double)A.max_p * (double)hd < lim &&
+      2.0 * (double)hd * (double)A.sum_p2 < lim) {
+    b.attn_flops = i2d(2 * hd * A.sum_p2);
+  } else {
+    double total = 0.0;
+    if (I.lane == 0) {
+      const int32_t* il = ilist(I, r);
+      for (int i = 0; i < A.m; i++) {
+        const int64_t p = P.prompt[gi(I, il[i])];
+        total = total + attention_prefill_term(p, p, hd);
+      }
+    }
+    b.attn_flops = __shfl_sync(FS_FULL, total, 0);
+  }
+#if FS_LEARNED
+  b.learned_attn = d->attn_forest != -1
+                       ? learned_attention_us(P, I, false, ilist(I, r), A.m, 0, rd.cost.tp, sm)
+                       : __longlong_as_double(0x7ff8000000000000LL);
+#endif
+  s.ilen = A.m;
+  launch_batch(P, I, r, s, rd, b, PH_PREFILL, sm);
+}
+
+__device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
+                             const fs_replica_desc& rd, WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  BatchShape b;
+  b.n_tokens = s.rlen;  // running <= max_num_seqs in every mode, so the batch is all of it
+  b.sum_q = s.rlen;
+  b.sum_kv = s.sum_ctx;
+  int hq, hkv;
+  heads_of(d, rd.cost.tp, hq, hkv);
+  b.attn_flops = attention_decode_flops(s.sum_ctx, (int64_t)hq * d->head_dim);
+#if FS_LEARNED
+  b.learned_attn = d->attn_forest != -1
+                       ? learned_attention_us(P, I, true, rlist(I, r), s.rlen, s.dstep, rd.cost.tp, sm)
+                       : __longlong_as_double(0x7ff8000000000000LL);
+#endif
+  launch_batch(P, I, r, s, rd, b, PH_DECODE, sm);
+}
+
+__device__ void kick(Inst& I, int r, RepState& s) {
+  if (s.busy || s.start_pending) return;
+  if (s.qlen == 0 && s.rlen == 0) return;
+  s.start_pending = 1;
+  heap_push(I, I.now, K_BATCH_START, r, 0);
+}
+
+// append requests (cooperatively: lane i holds req if has) to the running list
+__device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
+                               int req, int emitted) {
+  const unsigned lt = (1u << I.lane) - 1u;
+  const unsigned hm = __ballot_sync(FS_FULL, has);
+  int32_t* rl = rlist(I, r);
+  int64_t ctx = 0, fin = kNoFinish;
+  if (has) {
+    const int out = P.output[gi(I, req)];
+    const int32_t f = s.dstep + (out - emitted);
+    rl[s.rlen + __popc(hm & lt)] = req;
+    I.fin[req] = f;
+    ctx = (int64_t)P.prompt[gi(I, req)] + emitted;
+    fin = f;
+  }
+  s.rlen += __popc(hm);
+  s.sum_ctx += warp_sum_i64(ctx);
+  s.min_finish = (int32_t)min((int64_t)s.min_finish, warp_min_i64(fin));
+  __syncwarp();
+}
+
+// prefill completion (colocated.py:70-91, pd.py:98-112, af.py:514-535).
+// to_running: co-located / AF; otherwise PD (unfinished go to the transfer FIFO).
+__device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
+                                 bool to_running) {
+  const fs_instance_desc* d = I.d;
+  const int32_t* il = ilist(I, r);
+  const int nm = s.ilen;
+  const unsigned lt = (1u << I.lane) - 1u;
+  I.events += nm + 1;  // PREFILL_COMPLETE per member + one TOKEN_EMITTED
+  for (int base = 0; base < nm; base += 32) {
+    const int i = base + I.lane;
+    const bool valid = i < nm;
+    const int req = valid ? il[i] : 0;
+    const int out = valid ? P.output[gi(I, req)] : 0;
+    if (valid) P.first_ns[gi(I, req)] = I.now;
+    const bool fin = valid && out == 1;
+    const unsigned fm = __ballot_sync(FS_FULL, fin);
+    // completions and appends interleave in member order; they touch disjoint state
+    const int64_t fp = fin ? (to_running ? (int64_t)P.prompt[gi(I, req)] + out
+                                         : (int64_t)P.prompt[gi(I, req)]) : 0;
+    s.used -= warp_sum_i64(fin ? pool_rounded(d, fp) : 0);
+    if (fin) {
+      P.done_ns[gi(I, req)] = I.now;
+      P.done_rank[gi(I, req)] = I.n_done + __popc(fm & lt);
+    }
+    I.n_done += __popc(fm);
+    I.events += 2 * __popc(fm);
+    const bool keep = valid && !fin;
+    if (to_running) {
+      running_append(P, I, r, s, keep, req, 1);
+    } else {
+      const unsigned km = __ballot_sync(FS_FULL, keep);
+      if (keep) P.xfer[I.ro + (I.xt + __popc(km & lt)) % I.N] = req;
+      I.xt += __popc(km);
+    }
+    __syncwarp();
+  }
+}
+
+// decode / AF completion: every member emitted one token; finished requests leave
+// the running list in order (colocated.py:92-107, pd.py:113-127, af.py:536-551).
+// Returns the number finished. pool charge per finished request = rounded(prompt+output).
+__device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
+  const fs_instance_desc* d = I.d;
+  I.events += 1;  // TOKEN_EMITTED
+  s.dstep++;
+  s.sum_ctx += s.rlen;
+  if (s.min_finish != s.dstep) return 0;
+  int32_t* rl = rlist(I, r);
+  const unsigned lt = (1u << I.lane) - 1u;
+  int w = 0, nf = 0;
+  int64_t freed_ctx = 0, freed_pool = 0, new_min = kNoFinish;
+  for (int base = 0; base < s.rlen; base += 32) {
+    const int i = base + I.lane;
+    const bool valid = i < s.rlen;
+    const int req = valid ? rl[i] : 0;
+    const int32_t f = valid ? I.fin[req] : kNoFinish;
+    const bool fin = valid && f == s.dstep;
+    const unsigned fm = __ballot_sync(FS_FULL, fin);
+    const unsigned km = __ballot_sync(FS_FULL, valid && !fin);
+    if (fin) {
+      const int64_t fp = (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)];
+      freed_ctx += fp;
+      freed_pool += pool_rounded(d, fp);
+      P.done_ns[gi(I, req)] = I.now;
+      P.done_rank[gi(I, req)] = I.n_done + __popc(fm & lt);
+    } else if (valid) {
+      new_min = min(new_min, (int64_t)f);
+    }
+    I.n_done += __popc(fm);
+    nf += __popc(fm);
+    __syncwarp();
+    if (valid && !fin) rl[w + __popc(km & lt)] = req;
+    w += __popc(km);
+    __syncwarp();
+  }
+  s.rlen = w;
+  s.sum_ctx -= warp_sum_i64(freed_ctx);
+  s.used -= warp_sum_i64(freed_pool);
+  s.min_finish = (int32_t)warp_min_i64(new_min);
+  I.events += 2 * nf;
+  return nf;
+}
+
+// ---- co-located (colocated.py) ------------------------------------------------------------------
+__device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
+  const int r = I.rr % I.R;
+  I.rr++;
+  RepState s = load_rep(P, I, r);
+  enqueue(P, I, r, s, req);
+  kick(I, r, s);
+  store_rep(P, I, r, s);
+}
+
+__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+                              WarpSmem* sm);
+
+__device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+  RepState s = load_rep(P, I, r);
+  s.start_pending = 0;
+  if (!s.busy) {
+    const fs_replica_desc rd = P.reps[I.rb + r];
+    const Admit A = admit_prefill(P, I, r, s, true, s.rlen, rd.kv_pool_tokens);
+    if (A.m) {
+      s.used += A.charge;
+      start_prefill(P, I, r, s, rd, A, sm);
+    } else if (s.rlen) {
+      if (I.mode == FS_MODE_AF) af_start_step(P, I, s, rd, sm);
+      else start_decode(P, I, r, s, rd, sm);
+    } else if (s.qlen) {
+      fail(I, FS_ERR_REQUEST_CANNOT_FIT, queue_head(I, r, s));
+    }
+  }
+  store_rep(P, I, r, s);
+}
+
+__device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+  RepState s = load_rep(P, I, r);
+  s.busy = 0;
+  s.busy_ns += dur;
+  if (s.inflight_phase == PH_PREFILL) {
+    log_batch(P, I, r, PH_PREFILL, dur, ilist(I, r), s.ilen, s.inflight_moe);
+    I.prefill_batches++;
+    prefill_complete(P, I, r, s, true);
+  } else {
+    log_batch(P, I, r, s.inflight_phase, dur, rlist(I, r), s.rlen, s.inflight_moe);
+    if (s.inflight_phase == PH_AF) I.af_steps++; else I.decode_batches++;
+    decode_complete(P, I, r, s);
+  }
+  kick(I, r, s);
+  store_rep(P, I, r, s);
+}
+
+// ---- PD (pd.py) ---------------------------------------------------------------------------------
+// argmin over replicas of `role` by (key value, key_rank); value from rstate
+__device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
+  int64_t best_v = INT64_MAX;
+  int best_rank = 0x7fffffff, best_r = -1;
+  for (int r = I.lane; r < I.R; r += 32) {
+    const fs_replica_desc& rd = P.reps[I.rb + r];
+    if (rd.role != role) continue;
+    const RepState& st = I.rs[r];
+    const int64_t v = by_used ? st.used : st.outstanding;
+    if (v < best_v || (v == best_v && rd.key_rank < best_rank)) {
+      best_v = v; best_rank = rd.key_rank; best_r = r;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t ov = __shfl_xor_sync(FS_FULL, best_v, o);
+    const int ok = __shfl_xor_sync(FS_FULL, best_rank, o);
+    const int orr = __shfl_xor_sync(FS_FULL, best_r, o);
+    if (ov < best_v || (ov == best_v && ok < best_rank)) { best_v = ov; best_rank = ok; best_r = orr; }
+  }
+  return best_r;
+}
+
+__device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
+  __syncwarp();
+  const int r = pd_pick(P, I, FS_ROLE_PREFILL, false);
+  RepState s = load_rep(P, I, r);
+  if (I.lane == 0) P.home[gi(I, req)] = r;
+  enqueue(P, I, r, s, req);
+  s.outstanding += P.prompt[gi(I, req)];
+  kick(I, r, s);
+  store_rep(P, I, r, s);
+}
+
+// _pump_transfers (pd.py:141-192): strict FIFO, decode replica by (used, key)
+__device__ void pd_pump(const EngineParams& P, Inst& I) {
+  const fs_instance_desc* d = I.d;
+  while (I.xt > I.xh && I.status == FS_OK) {
+    const int req = P.xfer[I.ro + I.xh % I.N];
+    const int r = pd_pick(P, I, FS_ROLE_DECODE, true);
+    RepState s = load_rep(P, I, r);
+    const int64_t cap = P.reps[I.rb + r].kv_pool_tokens;
+    const int64_t prompt = P.prompt[gi(I, req)];
+    const int64_t fp = pool_rounded(d, prompt + P.output[gi(I, req)]);
+    if (fp > cap) { fail(I, FS_ERR_REQUEST_CANNOT_FIT, req); return; }
+    if (fp > cap - s.used) return;  // Backpressure: wait for decode memory
+    s.used += fp;
+    store_rep(P, I, r, s);
+    I.xh++;
+    I.events += 1;  // KV_CACHE_TRANSFER_START
+    const int64_t nbytes = d->kv_bytes_per_token * prompt;
+    const double sec = d->inter_latency_s + i2d(nbytes) / d->inter_bandwidth_bps;
+    heap_push(I, I.now + py_round(sec * 1e9), K_KV_DONE, r, req);
+  }
+}
+
+__device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  RepState s = load_rep(P, I, r);
+  s.start_pending = 0;
+  if (!s.busy) {
+    const fs_replica_desc rd = P.reps[I.rb + r];
+    if (rd.role == FS_ROLE_PREFILL) {
+      const Admit A = admit_prefill(P, I, r, s, false, 0, rd.kv_pool_tokens);
+      if (A.m == 0) {
+        if (s.qlen && s.used == 0) fail(I, FS_ERR_REQUEST_CANNOT_FIT, queue_head(I, r, s));
+      } else {
+        s.used += A.charge;
+        s.outstanding -= A.sum_p;
+        start_prefill(P, I, r, s, rd, A, sm);
+      }
+    } else {
+      // queue -> running up to max_num_seqs (pd.py:89-96)
+      const int take = min(s.qlen, max(0, d->max_num_seqs - s.rlen));
+      int32_t* q = qlist(I, r);
+      for (int base = 0; base < take; base += 32) {
+        const int i = base + I.lane;
+        const bool has = i < take;
+        running_append(P, I, r, s, has, has ? q[i] : 0, 1);
+      }
+      list_drop_front(q, s.qlen, take, I.lane);
+      s.qlen -= take;
+      if (s.rlen) start_decode(P, I, r, s, rd, sm);
+    }
+  }
+  store_rep(P, I, r, s);
+}
+
+__device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+  RepState s = load_rep(P, I, r);
+  s.busy = 0;
+  s.busy_ns += dur;
+  if (s.inflight_phase == PH_PREFILL) {
+    log_batch(P, I, r, PH_PREFILL, dur, ilist(I, r), s.ilen, s.inflight_moe);
+    I.prefill_batches++;
+    prefill_complete(P, I, r, s, false);
+    store_rep(P, I, r, s);
+    pd_pump(P, I);
+  } else {
+    log_batch(P, I, r, PH_DECODE, dur, rlist(I, r), s.rlen, s.inflight_moe);
+    I.decode_batches++;
+    const int nf = decode_complete(P, I, r, s);
+    store_rep(P, I, r, s);
+    if (nf) pd_pump(P, I);
+  }
+  s = load_rep(P, I, r);
+  kick(I, r, s);
+  store_rep(P, I, r, s);
+}
+
+__device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
+  const fs_instance_desc* d = I.d;
+  I.events += 1;  // MEMORY_AVAILABLE
+  __syncwarp();
+  const int ph = P.home[gi(I, req)];
+  RepState sp = load_rep(P, I, ph);
+  sp.used -= pool_rounded(d, P.prompt[gi(I, req)]);
+  store_rep(P, I, ph, sp);
+  RepState sd = load_rep(P, I, dr);
+  __syncwarp();
+  if (I.lane == 0) qlist(I, dr)[sd.qlen] = req;
+  sd.qlen++;
+  store_rep(P, I, dr, sd);
+  sp = load_rep(P, I, ph);
+  kick(I, ph, sp);
+  store_rep(P, I, ph, sp);
+  sd = load_rep(P, I, dr);
+  kick(I, dr, sd);
+  store_rep(P, I, dr, sd);
+}
+
+// ---- AF step (af.py:244-319, 468-507) ------------------------------------------------------------
+__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+                              WarpSmem* sm) {
+  const fs_instance_desc* d = I.d;
+  const int L = d->num_layers;
+  const int B = s.rlen;
+  const int m = min(d->af_micro_batches, B);
+  if (m > FS_MAX_MICRO_BATCHES) { fail(I, FS_ERR_CAPACITY, m); return; }
+  const int64_t step = I.af_counter++;
+  const int32_t* rl = rlist(I, 0);
+  const fs_cost_ctx ca = d->af_attn, cf = d->af_ffn;
+  int hq, hkv;
+  heads_of(d, ca.tp, hq, hkv);
+  const int64_t hd = (int64_t)hq * d->head_dim;
+  const int base = B / m, rem = B % m;
+  int64_t* ffn = P.af_ffn + P.af_base[I.idx];
+  int off = 0;
+  for (int i = 0; i < m; i++) {
+    const int sz = base + (i < rem ? 1 : 0);
+    // attention: largest attn_dp group = first ceil(sz / min(dp, sz)) members
+    const int g = min(d->af_attn_dp, sz);
+    const int w = sz / g + (sz % g ? 1 : 0);
+    int64_t ctx = 0;
+    for (int j = I.lane; j < w; j += 32) {
+      const int req = rl[off + j];
+      ctx += (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)] + s.dstep - I.fin[req];
+    }
+    ctx = warp_sum_i64(ctx);
+#if FS_LEARNED
+    const double att =
+        d->attn_forest != -1
+            ? learned_attention_us(P, I, true, rl + off, w, s.dstep, ca.tp, sm)
+            : attn_cost_us(d, ca, attention_decode_flops(ctx, hd), w, ctx);
+#else
+    const double att = attn_cost_us(d, ca, attention_decode_flops(ctx, hd), w, ctx);
+#endif
+    double us = qkv_us(d, ca, w) + att;
+    us = us + out_us(d, ca, w);
+    us = us + tpcoll_us(d, ca, w);
+    const int64_t attn_ns = py_round(us * 1000.0);
+    const int64_t nb = (int64_t)sz * d->d_model * d->dtype_bytes;
+    const double sec = d->inter_latency_s + i2d(nb) / d->inter_bandwidth_bps;
+    const int64_t xfer_ns = py_round(sec * 1e9);
+    if (I.lane == 0) {
+      sm->af_attn[i] = attn_ns;
+      sm->af_xfer[i] = xfer_ns;
+      sm->af_size[i] = sz;
+    }
+    // FFN durations per layer (af.py:289-301): MoE routes with the uniform policy
+    if (!d->has_moe) {
+      double f = FFN_DENSE_US(cf, sz);
+      f = f + tpcoll_us(d, cf, sz);
+      const int64_t fns = py_round(f * 1000.0);
+      for (int k = I.lane; k < L; k += 32) ffn[(int64_t)i * L + k] = fns;
+    } else {
+      const bool board = use_job_board(d, FS_ROUTE_UNIFORM, sz);
+      for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
+        const int lend = min(L, l0 + kLayerChunk);
+        if (board) {
+          int st = run_route_job(P, I, rd.prefix_mb, i + 1, step, l0, lend - l0, sz);
+          double lane_f = 0.0;
+          if (st == FS_OK)
+            st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, sz, d->num_experts,
+                                  d->top_k, d->d_model, d->expert_d_ff, d->ffn_matrices,
+                                  d->dtype_bytes, cf.ep, cf.moe_tp, d->intra_latency_s,
+                                  d->intra_bandwidth_bps, cf, &lane_f, nullptr);
+          if (st != FS_OK) { fail(I, st, l0); return; }
+          if (I.lane < lend - l0) ffn[(int64_t)i * L + l0 + I.lane] = py_round(lane_f * 1000.0);
+          I.routing_calls += lend - l0;
+          if (P.log_enabled && P.log.routes) {
+            for (int l = l0; l < lend; l++) {
+              load_job_layer(P, I, l - l0, sm);
+              log_route(P, I, 0, i + 1, step, l, sz, sm);
+            }
+          }
+          __syncwarp();
+          continue;
+        }
+        derive_layer_keys(P, I, rd.prefix_mb, i + 1, step, l0, L, sm);
+        for (int l = l0; l < lend; l++) {
+          int st = route_layer(P, I, FS_ROUTE_UNIFORM, sz, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
+          if (st != FS_OK) { fail(I, st, l); return; }
+          I.routing_calls++;
+          log_route(P, I, 0, i + 1, step, l, sz, sm);
+          double f;
+          st = moe_layer_warp(I.lane, sm->counts, sz, d->num_experts, d->top_k, d->d_model,
+                              d->expert_d_ff, d->ffn_matrices, d->dtype_bytes, cf.ep, cf.moe_tp,
+                              d->intra_latency_s, d->intra_bandwidth_bps, cf, &f, nullptr);
+          if (st != FS_OK) { fail(I, st, l); return; }
+          __syncwarp();
+          if (I.lane == 0) ffn[(int64_t)i * L + l] = py_round(f * 1000.0);
+        }
+      }
+    }
+    off += sz;
+  }
+  __syncwarp();
+  // list scheduling over 4 exclusive resources; lowest micro-batch claims first;
+  // all completions at an instant are retired before dispatch (af.py:141-229)
+  int64_t final_ts = 0, attn_busy = 0, busy4[4] = {0, 0, 0, 0};
+  if (I.lane == 0) {
+    for (int i = 0; i < m; i++) sm->af_stage[i] = 0;
+    unsigned long long ready[4] = {0, 0, 0, 0};
+    ready[0] = (m == 64) ? ~0ull : ((1ull << m) - 1ull);
+    int busy_mb[4] = {-1, -1, -1, -1};
+    int64_t endt[4] = {0, 0, 0, 0};
+    int64_t t = 0;
+    for (;;) {
+      for (int res = 0; res < 4; res++) {
+        if (busy_mb[res] < 0 && ready[res]) {
+          const int i = __ffsll((long long)ready[res]) - 1;
+          ready[res] &= ready[res] - 1;
+          const int stg = sm->af_stage[i];
+          const int k = stg >> 2;
+          int64_t dur;
+          if (res == 0) dur = sm->af_attn[i];
+          else if (res == 2) dur = ffn[(int64_t)i * L + k];
+          else dur = sm->af_xfer[i];
+          busy_mb[res] = i;
+          endt[res] = t + dur;
+          busy4[res] += dur;
+        }
+      }
+      bool any = false;
+      int64_t tmin = INT64_MAX;
+      for (int res = 0; res < 4; res++)
+        if (busy_mb[res] >= 0) { any = true; tmin = min(tmin, endt[res]); }
+      if (!any) break;
+      t = tmin;
+      for (int res = 0; res < 4; res++) {
+        if (busy_mb[res] >= 0 && endt[res] == t) {
+          const int i = busy_mb[res];
+          busy_mb[res] = -1;
+          const int stg = sm->af_stage[i];
+          const int k = stg >> 2;
+          if (res == 2 && k == L - 1) {
+            sm->af_stage[i] = -1;
+            if (i == m - 1) final_ts = t;
+          } else {
+            const int nxt = stg + 1;
+            sm->af_stage[i] = nxt;
+            ready[nxt & 3] |= 1ull << i;
+          }
+        }
+      }
+    }
+    attn_busy = busy4[0];
+  }
+  final_ts = __shfl_sync(FS_FULL, final_ts, 0);
+  attn_busy = __shfl_sync(FS_FULL, attn_busy, 0);
+  for (int res = 0; res < 4; res++) I.af_busy[res] += __shfl_sync(FS_FULL, busy4[res], 0);
+  const int64_t dur = final_ts;
+  if (dur > 0) {
+    const int64_t idle = max((int64_t)0, dur - attn_busy);
+    I.bubble_weighted = I.bubble_weighted + (double)idle;
+    I.bubble_total += dur;
+  }
+  I.events += 4LL * m * L - m;  // node-completion events
+  s.busy = 1;
+  s.steps++;
+  s.inflight_phase = PH_AF;
+  s.inflight_dur = dur;
+  s.inflight_moe = 0;
+  heap_push(I, I.now + dur, K_BATCH_COMPLETE, 0, dur);
+}
+
+// ---- the per-instance event loop -------------------------------------------------------------------
+// Bytes of per-instance hot state (replica states, event heap, queue / running /
+// inflight lists, finish steps); kept in the warp's shared-memory slab when it
+// fits, in HBM otherwise (generic pointers make both paths the same code).
+__device__ __forceinline__ int64_t slab_need(int R, int N) {
+  const int64_t rs = (int64_t)R * sizeof(RepState);
+  const int64_t heap = ((int64_t)R + N + 8) * sizeof(HEv);
+  const int64_t lists = 3LL * R * (N > 0 ? N : 1) * 4;
+  const int64_t fin = ((int64_t)N * 4 + 15) / 16 * 16;
+  return rs + heap + lists + fin;
+}
+
+__device__ void simulate_instance(const EngineParams& P, int idx, int lane, int slot, WarpSmem* sm,
+                                  char* slab) {
+  const long long t_start = clock64();
+  Inst I;
+  const fs_instance_desc* d = &P.descs[idx];
+  I.d = d;
+  I.idx = idx;
+  I.lane = lane;
+  I.slot = slot;
+  I.N = d->n_requests;
+  I.R = d->n_replicas;
+  I.mode = d->mode;
+  I.ro = d->req_offset;
+  I.rb = d->replica_offset;
+  if (slab && slab_need(I.R, I.N) <= kSlabBytes) {
+    char* p = slab;
+    I.rs = reinterpret_cast<RepState*>(p);
+    p += (int64_t)I.R * sizeof(RepState);
+    I.heap = reinterpret_cast<HEv*>(p);
+    p += ((int64_t)I.R + I.N + 8) * sizeof(HEv);
+    I.fin = reinterpret_cast<int32_t*>(p);
+    p += ((int64_t)I.N * 4 + 15) / 16 * 16;
+    I.lists = reinterpret_cast<int32_t*>(p);
+  } else {
+    I.rs = P.rstate + I.rb;
+    I.heap = P.heap + P.heap_base[idx];
+    I.fin = P.finish_at + I.ro;
+    I.lists = P.lists + P.list_base[idx];
+  }
+  I.hn = 0;
+  I.now = 0;
+  I.seq = 0;
+  I.events = 0;
+  I.max_events = d->max_events;
+  I.rr = 0; I.n_done = 0; I.cursor = 0;
+  I.status = FS_OK; I.detail = 0;
+  I.xh = 0; I.xt = 0;
+  I.af_counter = 0;
+  for (int k = 0; k < 4; k++) I.af_busy[k] = 0;
+  I.bubble_weighted = 0.0;
+  I.bubble_total = 0;
+  I.prefill_batches = I.decode_batches = I.af_steps = I.moe_samples = I.routing_calls = 0;
+  I.log_batches = I.log_moff = I.log_eoff = I.log_routes = 0;
+
+  if (I.R > FS_MAX_REPLICAS || (d->has_moe && d->num_experts > FS_MAX_EXPERTS)) fail(I, FS_ERR_CAPACITY, 0);
+#if FS_LEARNED
+  // learned grouped GEMM on MoE layers needs numpy's np.log (load entropy): next
+  if (d->has_moe && d->gg_forest != -1) fail(I, FS_ERR_UNSUPPORTED, 101);
+  {
+    const int fsel[2] = {d->attn_forest, d->gg_forest};
+    for (int k = 0; k < 2; k++) {
+      if (fsel[k] >= P.fv.n_forests || fsel[k] < -2) fail(I, FS_ERR_INTERNAL, 7);
+      if (fsel[k] >= 0 && fsel[k] < P.fv.n_forests) {
+        const int nt = P.fv.forests[fsel[k]].n_trees;
+        if (nt < 1 || nt > kMaxForestTrees) fail(I, FS_ERR_CAPACITY, nt);
+      }
+    }
+  }
+#else
+  // the host picks the learned variant for any instance with a model
+  if (d->attn_forest != -1 || d->gg_forest != -1) fail(I, FS_ERR_INTERNAL, 8);
+#endif
+  for (int r = lane; r < I.R; r += 32) {
+    RepState s;
+    s.used = 0; s.outstanding = 0; s.steps = 0; s.busy_ns = 0; s.sum_ctx = 0; s.inflight_dur = 0;
+    s.qlen = 0; s.rlen = 0; s.ilen = 0; s.busy = 0; s.start_pending = 0; s.dstep = 0;
+    s.min_finish = kNoFinish; s.inflight_phase = 0; s.inflight_moe = 0; s.pad = 0;
+    I.rs[r] = s;
+  }
+  __syncwarp();
+
+  while (I.status == FS_OK) {
+    const bool have_arr = I.cursor < I.N;
+    const bool have_ev = I.hn > 0;
+    if (!have_arr && !have_ev) break;
+    const int64_t ta = have_arr ? P.arrival[I.ro + I.cursor] : INT64_MAX;
+    const int64_t te = have_ev ? heap_top_t(I) : INT64_MAX;
+    I.events++;
+    if (I.events > I.max_events) { fail(I, FS_ERR_EVENT_BUDGET, 0); break; }
+    if (have_arr && ta <= te) {
+      I.now = ta;
+      const int req = I.cursor++;
+      if (I.mode == FS_MODE_PD) pd_arrival(P, I, req);
+      else co_arrival(P, I, req);
+    } else {
+      const HEv e = heap_pop(I);
+      I.now = e.t;
+      if (e.kind == K_BATCH_START) {
+        if (I.mode == FS_MODE_PD) pd_batch_start(P, I, e.a, sm);
+        else co_batch_start(P, I, e.a, sm);
+      } else if (e.kind == K_BATCH_COMPLETE) {
+        if (I.mode == FS_MODE_PD) pd_batch_complete(P, I, e.a, e.b);
+        else co_batch_complete(P, I, e.a, e.b);
+      } else if (e.kind == K_KV_DONE) {
+        pd_transfer_done(P, I, e.a, (int)e.b);
+      }
+    }
+  }
+  if (I.status == FS_OK && I.events > I.max_events) fail(I, FS_ERR_EVENT_BUDGET, 0);
+  if (I.status == FS_OK && I.n_done != I.N) fail(I, FS_ERR_SIMULATION, I.N - I.n_done);
+
+  __syncwarp();
+  if (lane == 0) {
+    fs_metric_row& row = P.rows[idx];
+    row.status = I.status;
+    row.status_detail = I.detail;
+    row.events = I.events;
+    row.prefill_batches = I.prefill_batches;
+    row.decode_batches = I.decode_batches;
+    row.af_steps = I.af_steps;
+    row.iterations = I.prefill_batches + I.decode_batches + I.af_steps;
+    row.routing_calls = I.routing_calls;
+    row.moe_layer_samples = d->has_moe ? (I.prefill_batches + I.decode_batches) * (int64_t)d->num_layers : 0;
+    row.n_requests = I.N;
+    for (int k = 0; k < 4; k++) row.af_busy_ns[k] = I.af_busy[k];
+    row.bubble_fraction = (I.mode == FS_MODE_AF && I.af_steps > 0)
+                              ? (I.bubble_total ? I.bubble_weighted / (double)I.bubble_total : 0.0)
+                              : __longlong_as_double(0x7ff8000000000000LL);
+    if (P.log_enabled) {
+      if (P.log.batch_count) P.log.batch_count[idx] = I.log_batches;
+      if (P.log.route_count) P.log.route_count[idx] = I.log_routes;
+    }
+    if (P.inst_cycles) P.inst_cycles[idx] = clock64() - t_start;
+  }
+  for (int r = lane; r < I.R; r += 32) {
+    const RepState s = I.rs[r];
+    fs_replica_out o;
+    o.busy_ns = s.busy_ns;
+    o.busy_fraction = 0.0;
+    o.steps_executed = s.steps;
+    P.rep_out[I.rb + r] = o;
+  }
+  __syncwarp();
+  if (lane == 0 && P.inst_done) atomicAdd(P.inst_done, 1);
+}
+
+#ifndef FS_SIM_MIN_BLOCKS
+#define FS_SIM_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerCta, FS_SIM_MIN_BLOCKS) sim_kernel(EngineParams P) {
+  __shared__ WarpSmem smem[kWarpsPerCta];
+  extern __shared__ __align__(16) char slabs[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem* sm = &smem[w];
+  char* slab = slabs + (int64_t)w * kSlabBytes;
+  for (;;) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(P.work_counter, 1);
+    k = __shfl_sync(FS_FULL, k, 0);
+    if (k >= P.n_inst) break;
+    simulate_instance(P, P.order[k], lane, blockIdx.x * kWarpsPerCta + w, sm, slab);
+  }
+  if (P.jobs) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w);
+}
+
+// Persistent grid: every CTA resident at once (the job board relies on warps
+// that run out of instances turning into helpers; correctness does not).
+static size_t sim_dyn_smem() {
+  static bool configured = false;
+  const size_t bytes = (size_t)kWarpsPerCta * kSlabBytes;
+  if (!configured) {
+    cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    configured = true;
+  }
+  return bytes;
+}
+
+int slots(int n_sms, int n_inst) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel, 32 * kWarpsPerCta,
+                                                sim_dyn_smem());
+  if (per_sm < 1) per_sm = 1;
+  const int need = (n_inst + kWarpsPerCta - 1) / kWarpsPerCta;
+  int grid = n_sms * per_sm;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  return grid * kWarpsPerCta;
+}
+
+int launch(const EngineParams& p, void* stream) {
+  if (p.n_inst <= 0) return 0;
+  const int grid = p.n_slots / kWarpsPerCta;
+  sim_kernel<<<grid, 32 * kWarpsPerCta, sim_dyn_smem(), (cudaStream_t)stream>>>(p);
+  return 1;
+}
+
+}  // namespace FS_SIM_NS
+}  // namespace fs

@@ -58,6 +58,10 @@ def load_library(path: str = LIB_PATH):
         "fs_attention_features_dev": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp, vp]),
         "fs_route_uniform": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
         "fs_router_seeds": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i32, vp]),
+        "fs_set_forests": (ctypes.c_int, [vp, abi.ForestSetC]),
+        "fs_attention_forest": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i64, _AttnParamsC, vp]),
+        "fs_attention_forest_dev": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i64, _AttnParamsC,
+                                                   vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -204,6 +208,8 @@ class Engine:
                                     "(no CUDA device visible?)")
         self.h = h
         self.device = device
+        self._forests = None
+        self._staged = None
 
     def close(self) -> None:
         if getattr(self, "h", None):
@@ -226,7 +232,16 @@ class Engine:
         return int(self.lib.fs_last_launch_count(self.h))
 
     # -- batched simulation -------------------------------------------------------------
+    def set_forests(self, forests) -> None:
+        """Stage learned operator models (costmodel.ForestSet) in HBM; kept until replaced."""
+        from .costmodel import forest_set_struct
+        if forests is None or forests is self._forests:
+            return
+        self._check(self.lib.fs_set_forests(self.h, forest_set_struct(forests)), "fs_set_forests")
+        self._forests = forests
+
     def run(self, low: Lowered, log: LogSpec | None = None) -> RawResults:
+        self.set_forests(low.forests)
         res = alloc_results(low)
         if log is not None:
             res.log = make_log(low.n_instances, log)
@@ -241,6 +256,7 @@ class Engine:
         return res
 
     def stage(self, low: Lowered) -> None:
+        self.set_forests(low.forests)
         rc = self.lib.fs_stage(
             self.h, abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas), len(low.replicas),
             abi.ptr(low.prefixes), len(low.prefixes), abi.ptr(low.trace_counts),
@@ -291,6 +307,21 @@ class Engine:
         self._check(self.lib.fs_attention_features(self.h, abi.ptr(q), abi.ptr(kv),
                                                    abi.ptr(offsets), abi.ptr(is_decode), nb,
                                                    params, abi.ptr(out)), "fs_attention_features")
+        return out[:nb]
+
+    def attention_forest(self, forests, forest: int, q, kv, offsets, is_decode,
+                         params) -> np.ndarray:
+        """LearnedOperatorModel.predict_us(AttentionFeatures(...).vector()) per CSR batch."""
+        self.set_forests(forests)
+        q = np.ascontiguousarray(q, dtype=np.int32)
+        kv = np.ascontiguousarray(kv, dtype=np.int32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        is_decode = np.ascontiguousarray(is_decode, dtype=np.uint8)
+        nb = len(offsets) - 1
+        out = np.zeros(max(nb, 1), dtype=np.float64)
+        self._check(self.lib.fs_attention_forest(self.h, forest, abi.ptr(q), abi.ptr(kv),
+                                                 abi.ptr(offsets), abi.ptr(is_decode), nb,
+                                                 params, abi.ptr(out)), "fs_attention_forest")
         return out[:nb]
 
     def route_uniform(self, tokens, seeds, num_experts: int, top_k: int):

@@ -62,6 +62,14 @@ class EngineInternalError(RuntimeError):
 
 
 # enum fs_status (include/frontier_b200.h) -> exception type
+class ModelFileError(Exception):
+    """[costmodel/model.py:49] malformed or tampered operator-model file."""
+
+
+class SchemaMismatch(Exception):
+    """[costmodel/model.py:33] a model's feature schema does not fit its use."""
+
+
 STATUS_EXCEPTIONS = {
     1: RequestCannotFit,
     2: SimulationError,
@@ -76,4 +84,5 @@ STATUS_EXCEPTIONS = {
     11: EngineCapacityError,
     12: EngineInternalError,
     13: ValueError,
+    14: SchemaMismatch,
 }

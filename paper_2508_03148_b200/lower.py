@@ -18,6 +18,7 @@ import numpy as np
 
 from . import abi
 from .cluster import SchedulerPolicy
+from .costmodel import ForestSet, forest_slot
 from .errors import EngineCapacityError, SimulationError
 from .specs import AfPipelineConfig, RoutingPolicySpec
 from .topology import ClusterSpec, Deployment, kv_bytes_per_token
@@ -32,9 +33,15 @@ class InstanceSpec:
     af: AfPipelineConfig | None = None
     routing: RoutingPolicySpec = field(default_factory=RoutingPolicySpec)
     seed: int = 0
-    learned: bool = False
+    attention_model: object = None      # costmodel.LearnedModel | None
+    grouped_gemm_model: object = None   # costmodel.LearnedModel | None
     max_events: int = abi.DEFAULT_MAX_EVENTS
     tag: object = None
+
+
+    @property
+    def learned(self) -> bool:
+        return self.attention_model is not None or self.grouped_gemm_model is not None
 
 
 @dataclass
@@ -109,6 +116,7 @@ class Lowered:
     id_rank: np.ndarray
     replica_keys: list[list[str]]
     request_ids: list[list[str]]
+    forests: object = None  # costmodel.ForestSet | None (learned operator models)
 
     @property
     def n_instances(self) -> int:
@@ -128,6 +136,7 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
     arr_parts, p_parts, o_parts, rank_parts = [], [], [], []
     replica_keys, request_ids = [], []
     req_off = 0
+    forests = ForestSet()
     for i, sp in enumerate(specs):
         dep, model, pol = sp.deployment, sp.deployment.model, sp.policy
         pol.validate()
@@ -176,7 +185,12 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
         d["kv_bytes_per_token"] = kv_bytes_per_token(model)
         d["max_events"] = sp.max_events
         d["total_gpus"] = dep.total_gpus
-        d["cost_model_learned"] = 1 if sp.learned else 0
+        for slot, model, schema in (("attn_forest", sp.attention_model, "attention_v1"),
+                                    ("gg_forest", sp.grouped_gemm_model, "grouped_gemm_v1")):
+            if model is not None and model.schema == schema and model.n_trees > abi.MAX_FOREST_TREES:
+                raise EngineCapacityError(
+                    f"{model.path}: {model.n_trees} trees exceed {abi.MAX_FOREST_TREES}")
+            d[slot] = forest_slot(forests, model, schema)
         d["est_cost"] = _estimate_cost(sp)
         keys = [ri.key for ri in layout]
         key_rank = {k: r for r, k in enumerate(sorted(keys))}
@@ -223,4 +237,5 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
         trace_counts=np.asarray(trace if trace else [0], dtype=np.int64),
         arrival=cat(arr_parts, np.int64), prompt=cat(p_parts, np.int32),
         output=cat(o_parts, np.int32), id_rank=cat(rank_parts, np.int32),
-        replica_keys=replica_keys, request_ids=request_ids)
+        replica_keys=replica_keys, request_ids=request_ids,
+        forests=forests if forests.models else None)

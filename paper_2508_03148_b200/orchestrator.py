@@ -12,6 +12,7 @@ state timestamps), as the reference's handlers leave them.
 from __future__ import annotations
 
 from .cluster import SchedulerPolicy
+from .costmodel import check_model_slots_engine
 from .engine import Engine, LogSpec, default_engine
 from .errors import RequestCannotFit, SimulationError  # noqa: F401  (re-exported)
 from .lower import InstanceSpec, lower
@@ -57,6 +58,7 @@ class Simulation:
         policy.validate()
         if mode == "af":
             (af or AfPipelineConfig()).validate()
+        check_model_slots_engine(attention_model, grouped_gemm_model)
         self.mode = mode
         self.deployment = deployment
         self.requests = list(requests)
@@ -64,7 +66,7 @@ class Simulation:
         self.spec = InstanceSpec(
             deployment=deployment, requests=self.request_arrays, policy=policy,
             af=af if mode == "af" else None, routing=routing or RoutingPolicySpec(), seed=seed,
-            learned=attention_model is not None or grouped_gemm_model is not None,
+            attention_model=attention_model, grouped_gemm_model=grouped_gemm_model,
             max_events=50_000_000 if max_events is None else max_events)
         self._engine = engine
         self.log_routes = log_routes

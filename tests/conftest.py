@@ -47,6 +47,27 @@ def golden_c5():
 
 
 @pytest.fixture(scope="session")
+def model_dir(tmp_path_factory):
+    """The golden model files, uncompressed, as learned-mode configs name them."""
+    d = tmp_path_factory.mktemp("models")
+    for f in os.listdir(GOLDEN):
+        if f.startswith("forest_") and f.endswith(".json.gz") and f != "forest_predictions.json.gz":
+            with gzip.open(os.path.join(GOLDEN, f), "rb") as src:
+                (d / f[:-3]).write_bytes(src.read())
+    return str(d)
+
+
+@pytest.fixture(scope="session")
+def golden_learned():
+    return load_golden("learned_scenarios")["data"]
+
+
+@pytest.fixture(scope="session")
+def golden_forest_predictions():
+    return load_golden("forest_predictions")["data"]
+
+
+@pytest.fixture(scope="session")
 def engine():
     from paper_2508_03148_b200.engine import Engine
     return Engine(0)

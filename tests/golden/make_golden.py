@@ -228,9 +228,9 @@ class RouterRecorder:
         return False
 
 
-def record(doc: dict, with_batches: bool = True, with_routes: bool = False) -> dict:
+def record(doc: dict, with_batches: bool = True, with_routes: bool = False, base_dir: str = ".") -> dict:
     out: dict = {"config": doc}
-    config = parse_config(copy.deepcopy(doc))
+    config = parse_config(copy.deepcopy(doc), base_dir=base_dir)
     reqs = config.requests()
     out["requests"] = {
         "ids": [r.id for r in reqs],
@@ -399,6 +399,92 @@ def pure_function_vectors() -> dict:
     return vec
 
 
+def _save_model(name: str, model) -> str:
+    """Write `model` as tests/golden/{name}.json.gz and a plain copy under /tmp."""
+    path = os.path.join(HERE, f"{name}.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as fh:
+        json.dump(model.to_document(), fh, sort_keys=True, separators=(",", ":"))
+        fh.write("\n")
+    raw = os.path.join("/tmp", f"{name}.json")
+    with gzip.open(path, "rt", encoding="utf-8") as fh, open(raw, "w", encoding="utf-8") as g:
+        g.write(fh.read())
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+    return raw
+
+
+def forest_fixtures() -> dict:
+    """Learned operator models in the reference's model-file format
+    (model.py:140-182) plus reference predictions on C2-style batches."""
+    from frontier_sim.costmodel.features import AttentionFeatures
+    from frontier_sim.costmodel.forest import ForestHyperparams
+    from frontier_sim.costmodel.model import fit_model, load_model_file
+    from frontier_sim.costmodel.synthetic import (make_attention_suite, make_grouped_gemm_suite,
+                                                  sqrt_proxy_dataset)
+
+    out = {}
+    specs = {"forest_c2": (5000, None),                       # C2: 100 trees, depth 12
+             "forest_small": (1000, ForestHyperparams(n_trees=12, max_depth=8))}
+    for name, (n, hp) in specs.items():
+        suite, feats = make_attention_suite(n, seed=11, noise=0.03)
+        model, _ = fit_model(suite, hp, seed=7)
+        loaded = load_model_file(_save_model(name, model))
+        rng = np.random.default_rng(404)
+        preds = []
+        for b in range(512):
+            nreq = 72 if b % 5 else int(rng.integers(1, 300))
+            kv = np.clip(np.rint(rng.lognormal(6.5, 1.4, size=nreq)), 16, 32768).astype(int)
+            phase = "decode" if b % 2 == 0 else "prefill"
+            q = [1] * nreq if phase == "decode" else [int(x) for x in kv]
+            f = AttentionFeatures(phase, tuple(q), tuple(int(x) for x in kv), 32, 8, 128)
+            preds.append([phase, q, [int(x) for x in kv], loaded.predict_us(f.vector())])
+        out[name] = preds
+        if name == "forest_small":
+            # an attention-operator model on the wrong schema (SchemaMismatch at predict)
+            proxy, _ = fit_model(sqrt_proxy_dataset(suite, feats),
+                                 ForestHyperparams(n_trees=4, max_depth=4), seed=7)
+            _save_model("forest_sqrt_proxy", proxy)
+    # grouped-GEMM model (dense FFNs call it with one local expert, cluster.py:286-296)
+    suite, _ = make_grouped_gemm_suite(1500, seed=12, noise=0.02)
+    gg, _ = fit_model(suite, ForestHyperparams(n_trees=16, max_depth=10), seed=5)
+    _save_model("forest_gg_small", gg)
+    return out
+
+
+def learned_scenarios() -> dict[str, dict]:
+    """Scenarios whose operator costs come from the small learned forests."""
+    att = {"mode": "learned", "attention_model": "forest_small.json"}
+    gg = {"mode": "learned", "grouped_gemm_model": "forest_gg_small.json"}
+    both = {"mode": "learned", "attention_model": "forest_small.json",
+            "grouped_gemm_model": "forest_gg_small.json"}
+    s = {}
+    d = W.c1_colocated(40, seed=21)
+    d["cost_model"] = dict(att)
+    s["learned_co_llama_40"] = d
+    d = W.c3_pd(30, seed=22, tight=True)
+    d["cost_model"] = dict(att)
+    s["learned_pd_70b_tight_30"] = d
+    d = copy.deepcopy(scenarios()["af_tiny_moe_m3_dp2"])
+    d["seed"] = 23
+    d["cost_model"] = dict(att)
+    s["learned_af_tiny_moe"] = d
+    d = W.c1_colocated(40, seed=24)
+    d["cost_model"] = dict(gg)
+    s["learned_gg_co_llama_40"] = d
+    d = W.c3_pd(30, seed=25, tight=False)
+    d["cost_model"] = dict(both)
+    s["learned_both_pd_70b_30"] = d
+    d = W.c1_colocated(12, seed=26)
+    d["cost_model"] = {"mode": "learned", "attention_model": "forest_sqrt_proxy.json"}
+    s["learned_err_attention_schema"] = d
+    d = W.c1_colocated(12, seed=27)
+    d["cost_model"] = {"mode": "learned", "attention_model": "forest_gg_small.json"}
+    s["learned_err_operator_slot"] = d
+    d = W.c1_colocated(12, seed=28)
+    d["cost_model"] = {"mode": "analytic", "grouped_gemm_model": "forest_gg_small.json"}
+    s["learned_gg_mode_analytic_still_loads"] = d
+    return s
+
+
 def write(name: str, payload) -> None:
     payload = {"numpy": np.__version__, "python": sys.version.split()[0], "data": payload}
     path = os.path.join(HERE, f"{name}.json.gz")
@@ -425,6 +511,14 @@ def main() -> None:
             print(name, sc[name].get("iterations"), sc[name].get("error"),
                   f"{sc[name]['wall_s']:.2f}s")
         write("scenarios", sc)
+    if only is None or "forest" in only:
+        write("forest_predictions", forest_fixtures())
+        sc = {}
+        for name, doc in learned_scenarios().items():
+            sc[name] = record(doc, with_batches=True, with_routes="moe" in doc["model"],
+                              base_dir="/tmp")
+            print(name, sc[name].get("iterations"), sc[name].get("error"))
+        write("learned_scenarios", sc)
     if not args.skip_baseline and (only is None or "baseline" in only):
         bl = {}
         for name, doc in baseline_scenarios().items():

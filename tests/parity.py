@@ -13,13 +13,13 @@ from paper_2508_03148_b200.orchestrator import detail_log_spec
 PHASE = {"prefill": "prefill", "decode": "decode", "af_decode": "af_decode"}
 
 
-def specs_for(docs):
-    return [instance_spec(parse_config(copy.deepcopy(d))) for d in docs]
+def specs_for(docs, base_dir="."):
+    return [instance_spec(parse_config(copy.deepcopy(d), base_dir=base_dir)) for d in docs]
 
 
-def run_backend(backend, docs, routes=False, threads=1):
+def run_backend(backend, docs, routes=False, threads=1, base_dir="."):
     """backend: 'oracle' or an Engine."""
-    specs = specs_for(docs)
+    specs = specs_for(docs, base_dir)
     low = lower(specs)
     logs = [detail_log_spec(s, routes=routes) for s in specs]
     from paper_2508_03148_b200.engine import LogSpec
