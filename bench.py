@@ -212,33 +212,58 @@ def bench_attention_cost(eng, device: int, steps: int, warmup: int, n_batches: i
     prm = attn_params(32, 8, 128, 2, 2.25e15, 8e12, 5.0)
     stream = torch.cuda.Stream(device=device)
 
-    def launch():
-        eng.attention_cost_dev(tq.data_ptr(), tkv.data_ptr(), toff.data_ptr(), tdec.data_ptr(),
-                               n_batches, prm, out.data_ptr(), st.data_ptr(), stream.cuda_stream)
+    def time_launches(launch):
+        for _ in range(max(warmup, 1)):
+            launch()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        for s, e in ev:
+            s.record(stream)
+            launch()
+            e.record(stream)
+        torch.cuda.synchronize()
+        return sum(s.elapsed_time(e) for s, e in ev) / steps
 
-    for _ in range(max(warmup, 1)):
-        launch()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(steps)]
-    for s, e in ev:
-        s.record(stream)
-        launch()
-        e.record(stream)
-    torch.cuda.synchronize()
-    ms = sum(s.elapsed_time(e) for s, e in ev) / steps
+    ms = time_launches(lambda: eng.attention_cost_dev(
+        tq.data_ptr(), tkv.data_ptr(), toff.data_ptr(), tdec.data_ptr(), n_batches, prm,
+        out.data_ptr(), st.data_ptr(), stream.cuda_stream))
     n_el = int(off[-1])
     alg = 8 * n_el + 8 * (n_batches + 1) + n_batches + 8 * n_batches + 4 * n_batches
     peak, kind = measured_peaks()
     gbs = alg / (ms / 1e3) / 1e9
     ok = bool((st == 0).all().item())
-    return {"workload": f"{n_batches} batches x 72 requests, lognormal(6.5,1.4) kv lengths, "
-                        "alternating decode / prefill", "batches_per_s": n_batches / (ms / 1e3),
-            "ms_per_launch": ms, "algorithmic_bytes_per_launch": alg,
-            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
-                         "frac": gbs / peak, "traffic": ncu_traffic("attention_cost_kernel"),
-                         "peak_source": kind},
-            "all_status_ok": ok}
+    res = {"workload": f"{n_batches} batches x 72 requests, lognormal(6.5,1.4) kv lengths, "
+                       "alternating decode / prefill", "batches_per_s": n_batches / (ms / 1e3),
+           "ms_per_launch": ms, "algorithmic_bytes_per_launch": alg,
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                        "frac": gbs / peak, "traffic": ncu_traffic("attention_cost_kernel"),
+                        "peak_source": kind},
+           "all_status_ok": ok}
+    # learned mode: the C2 forest (make_attention_suite(5000, seed=11) -> fit_model(seed=7),
+    # 100 trees, depth <= 12) over the same batches: 17 features + 100 tree walks + sort
+    model_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden",
+                              "forest_c2.json.gz")
+    if os.path.exists(model_path):
+        from paper_2508_03148_b200.costmodel import ForestSet, load_model_file
+        fs = ForestSet()
+        fs.add(load_model_file(model_path))
+        eng.set_forests(fs)
+        out2 = torch.empty(n_batches, dtype=torch.float64, device=dev)
+        ms2 = time_launches(lambda: eng.attention_forest_dev(
+            0, tq.data_ptr(), tkv.data_ptr(), toff.data_ptr(), tdec.data_ptr(), n_batches, prm,
+            out2.data_ptr(), stream.cuda_stream))
+        alg2 = 8 * n_el + 8 * (n_batches + 1) + n_batches + 8 * n_batches
+        gbs2 = alg2 / (ms2 / 1e3) / 1e9
+        res["learned"] = {
+            "model": "forest_c2 (100 trees)", "batches_per_s": n_batches / (ms2 / 1e3),
+            "ms_per_launch": ms2, "algorithmic_bytes_per_launch": alg2,
+            "tree_walks_per_s": 100 * n_batches / (ms2 / 1e3),
+            "roofline": {"bound": "hbm", "achieved": gbs2, "peak": peak, "unit": "GB/s",
+                         "frac": gbs2 / peak, "traffic": ncu_traffic("attention_forest_kernel"),
+                         "peak_source": kind,
+                         "note": "tree walks are L2-latency bound; HBM fraction is low by design"}}
+    return res
 
 
 def main():

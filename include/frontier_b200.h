@@ -340,7 +340,9 @@ int fs_attention_features(fs_engine* e, const int32_t* q_lens, const int32_t* kv
 /* LearnedOperatorModel.predict_us(AttentionFeatures(...).vector()) over CSR
  * batches with staged forest `forest` (costmodel/model.py:126-136,
  * forest.py:234-239): 17 features, tree walks, sorted-leaf numpy mean,
- * max(., 1e-6). Device pointers, async on stream. */
+ * max(., 1e-6). A batch that fails AttentionFeatures' checks (empty, q < 1,
+ * decode q != 1, prefill kv < q, kv < 1; features.py:44-66) yields NaN.
+ * Device pointers, async on stream. */
 int fs_attention_forest_dev(fs_engine* e, int32_t forest, const int32_t* q_lens,
                             const int32_t* kv_lens, const int64_t* offsets,
                             const uint8_t* is_decode, int64_t n_batches, fs_attn_params params,

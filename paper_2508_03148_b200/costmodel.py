@@ -84,6 +84,12 @@ def load_model_file(path: str) -> LearnedModel:
                 rights.append(base + int(nd["right"]))
                 vals.append(0.0)
         base += len(nodes)
+    n_feat = SCHEMAS[doc["schema"]]
+    feat = np.asarray(feats, dtype=np.int64)
+    inner = feat >= 0
+    kids = np.concatenate([np.asarray(lefts)[inner], np.asarray(rights)[inner]])
+    if (feat[inner] >= n_feat).any() or (kids < 0).any() or (kids >= base).any():
+        raise ModelFileError(f"{path}: node feature or child index out of range")
     return LearnedModel(
         operator=doc["operator"], schema=doc["schema"], path=path, n_trees=len(roots),
         tree_root=np.asarray(roots, dtype=np.int64), feature=np.asarray(feats, dtype=np.int32),
@@ -218,4 +224,7 @@ def attention_cost_batches(q_lens, kv_lens, offsets, is_decode, num_query_heads,
     if model.schema != "attention_v1":
         raise SchemaMismatch(f"attention predictor uses schema {model.schema!r}; expected attention_v1")
     fs = ForestSet([model])
-    return eng.attention_forest(fs, 0, q_lens, kv_lens, offsets, is_decode, prm)
+    out = eng.attention_forest(fs, 0, q_lens, kv_lens, offsets, is_decode, prm)
+    if np.isnan(out).any():
+        raise ValueError(f"{int(np.isnan(out).sum())} batches failed AttentionFeatures validation")
+    return out

@@ -55,7 +55,7 @@ struct fs_engine {
   DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
       c_layers, c_seeds, c_pf, c_mid;
   // learned models (persist across stages)
-  DevBuf f_descs, f_roots, f_feature, f_threshold, f_left, f_right, f_value;
+  DevBuf f_descs, f_roots, f_right, f_value, f_leaf;  // f_value: packed NodeP array
   fs::ForestView fv{};
   bool learned = false;  // staged batch uses the learned simulation variant
   int32_t n_inst = 0, n_reps = 0, n_prefixes = 0;
@@ -496,22 +496,55 @@ int fs_set_forests(fs_engine* e, fs_forest_set f) {
       return 12;
     }
   }
+  // pack (threshold | leaf value, feature, left) into 16-byte nodes
+  std::vector<fs::NodeP> packed((size_t)f.n_nodes);
+  int consecutive = 1;
+  for (int64_t i = 0; i < f.n_nodes; i++) {
+    const bool leaf = f.feature[i] < 0;
+    packed[i].v = leaf ? f.value[i] : f.threshold[i];
+    packed[i].feature = f.feature[i];
+    packed[i].left = f.left[i];
+    if (!leaf) {
+      if (f.feature[i] >= 17 || f.left[i] < 0 || f.left[i] >= f.n_nodes || f.right[i] < 0 ||
+          f.right[i] >= f.n_nodes) {
+        e->err = "forest node " + std::to_string(i) + ": feature or child index out of range";
+        return 12;
+      }
+      if (f.right[i] != f.left[i] + 1) consecutive = 0;
+    }
+  }
+  // leaf value ranks: the device sorts 32-bit ranks instead of fp64 values
+  std::vector<double> leafv;
+  for (int64_t i = 0; i < f.n_nodes; i++)
+    if (f.feature[i] < 0) leafv.push_back(f.value[i]);
+  std::sort(leafv.begin(), leafv.end());
+  for (int64_t i = 0; i < f.n_nodes; i++)
+    if (f.feature[i] < 0) {
+      if (!(f.value[i] == f.value[i])) {
+        e->err = "forest node " + std::to_string(i) + ": NaN leaf value";
+        return 12;
+      }
+      packed[i].left =
+          (int32_t)(std::lower_bound(leafv.begin(), leafv.end(), f.value[i]) - leafv.begin());
+    }
+  for (int64_t t = 0; t < f.n_trees; t++)
+    if (f.tree_root[t] < 0 || f.tree_root[t] >= f.n_nodes) {
+      e->err = "forest tree " + std::to_string(t) + ": root out of range";
+      return 12;
+    }
   FS_CHECK(upload(e->f_descs, f.forests, (size_t)f.n_forests, s));
   FS_CHECK(upload(e->f_roots, f.tree_root, (size_t)f.n_trees, s));
-  FS_CHECK(upload(e->f_feature, f.feature, (size_t)f.n_nodes, s));
-  FS_CHECK(upload(e->f_threshold, f.threshold, (size_t)f.n_nodes, s));
-  FS_CHECK(upload(e->f_left, f.left, (size_t)f.n_nodes, s));
+  FS_CHECK(upload(e->f_value, packed.data(), packed.size(), s));
   FS_CHECK(upload(e->f_right, f.right, (size_t)f.n_nodes, s));
-  FS_CHECK(upload(e->f_value, f.value, (size_t)f.n_nodes, s));
+  FS_CHECK(upload(e->f_leaf, leafv.data(), leafv.size(), s));
   FS_CHECK(cudaStreamSynchronize(s));
   e->fv.forests = e->f_descs.as<fs_forest_desc>();
   e->fv.n_forests = f.n_forests;
+  e->fv.consecutive = consecutive;
   e->fv.tree_root = e->f_roots.as<int64_t>();
-  e->fv.feature = e->f_feature.as<int32_t>();
-  e->fv.threshold = e->f_threshold.as<double>();
-  e->fv.left = e->f_left.as<int32_t>();
+  e->fv.nodes = e->f_value.as<fs::NodeP>();
   e->fv.right = e->f_right.as<int32_t>();
-  e->fv.value = e->f_value.as<double>();
+  e->fv.leaf_by_rank = e->f_leaf.as<double>();
   e->params.fv = e->fv;
   return 0;
 }

@@ -446,12 +446,16 @@ __global__ void __launch_bounds__(32 * kForestWarps) attention_forest_kernel(
     auto fq = [&](int64_t i) -> int64_t { return q[o0 + i]; };
     auto fk = [&](int64_t i) -> int64_t { return kv[o0 + i]; };
     double x[17];
+    int bad;
     attention_features_w(d, n, fq, fk, prm.num_query_heads, prm.num_kv_heads, prm.head_dim, lane,
-                         x);
-    if (lane < 17) {
+                         x, &bad);
+    if (bad != FS_OK) {  // EmptyBatch / ValueError in AttentionFeatures.__post_init__
+      if (lane == 0) out[b] = __longlong_as_double(0x7ff8000000000000LL);
+      continue;
+    }
+    if (lane == 0) {
 #pragma unroll
-      for (int j = 0; j < 17; j++)
-        if (j == lane) sx[w][j] = x[j];
+      for (int j = 0; j < 17; j++) sx[w][j] = x[j];
     }
     __syncwarp();
     const double v = forest_predict_w(fv, forest, sx[w], svals[w], lane);

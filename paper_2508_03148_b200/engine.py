@@ -324,6 +324,13 @@ class Engine:
                                                  params, abi.ptr(out)), "fs_attention_forest")
         return out[:nb]
 
+    def attention_forest_dev(self, forest: int, q_ptr, kv_ptr, off_ptr, dec_ptr, nb, params,
+                             out_ptr, stream_ptr) -> None:
+        """Device-pointer form of attention_forest (models staged with set_forests)."""
+        self._check(self.lib.fs_attention_forest_dev(self.h, forest, q_ptr, kv_ptr, off_ptr,
+                                                     dec_ptr, nb, params, out_ptr, stream_ptr),
+                    "fs_attention_forest_dev")
+
     def route_uniform(self, tokens, seeds, num_experts: int, top_k: int):
         tokens = np.ascontiguousarray(tokens, dtype=np.int64)
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)

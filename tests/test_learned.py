@@ -102,7 +102,7 @@ def test_gpu_forest_predictions(engine, model_dir, golden_forest_predictions, na
     hw = SimpleNamespace(peak_flops=2.25e15, mem_bw=8.0e12, kernel_overhead_us=5.0)
     got = costmodel.attention_cost_batches(q, kv, off, dec, 32, 8, 128, hw, model=model,
                                            engine=engine)
-    assert engine.last_launch_count() >= 1
+    assert engine.last_launch_count >= 1
     assert got.tolist() == want.tolist()
 
 
@@ -122,7 +122,7 @@ def test_gpu_learned_mixed_batch_matches_oracle(engine, model_dir, golden_learne
     from test_gpu_parity import assert_same_raw
     from paper_2508_03148_b200.lower import lower
     from oracle import oracle
-    docs = [golden_learned[n]["config"] for n in RUNNABLE] + \
+    docs = [golden_learned[n]["config"] for n in RUNNABLE if "error" not in golden_learned[n]] + \
         [W.c1_colocated(30, seed=s) for s in range(3)]
     low = lower(specs_for(docs, model_dir))
     assert_same_raw(engine.run(low), oracle.run(low, threads=4))
