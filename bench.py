@@ -172,7 +172,10 @@ def ncu_traffic(kernel: str):
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+        for name, v in d.items():  # kernel variants carry a suffix (e.g. _tpb)
+            if name == kernel or name.startswith(kernel + "_"):
+                return v.get("dram_bytes_per_launch")
+        return None
     except Exception:
         return None
 

@@ -82,8 +82,8 @@ enum fs_status {
   FS_ERR_INVALID_TOPK = 8,         /* costmodel/routing.py:21 InvalidTopK                 */
   FS_ERR_ROUTING_TIE = 9,          /* exact key tie at the top-k boundary: argpartition's
                                       choice is implementation-defined; flagged, not guessed */
-  FS_ERR_UNSUPPORTED = 10,         /* feature not on the device path yet (dirichlet_skew,
-                                      learned grouped GEMM on MoE layers)                  */
+  FS_ERR_UNSUPPORTED = 10,         /* feature not on the device path yet (learned grouped
+                                      GEMM on MoE layers)                                  */
   FS_ERR_CAPACITY = 11,            /* engine limit (FS_MAX_*) exceeded                     */
   FS_ERR_INTERNAL = 12,            /* invariant violated inside the engine                 */
   FS_ERR_VALUE = 13,               /* ValueError raised by a cost-model argument check     */
@@ -356,6 +356,13 @@ int fs_attention_forest(fs_engine* e, int32_t forest, const int32_t* q_lens,
  * counts_out: n_calls x num_experts int32. status: per call. */
 int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
                      int32_t num_experts, int32_t top_k, int32_t* counts_out, int32_t* status);
+
+/* route_tokens(T, E, k, policy, seed, alpha) for a list of calls (host buffers):
+ * policy FS_ROUTE_UNIFORM or FS_ROUTE_DIRICHLET (routing.py:65-113; the trace
+ * policy needs no device). counts_out: n_calls x num_experts int32. status: per call. */
+int fs_route_tokens(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
+                    int32_t num_experts, int32_t top_k, int32_t policy, double alpha,
+                    int32_t* counts_out, int32_t* status);
 
 /* derive_router_seed for (prefix, step, layer[, micro_batch]) tuples (host buffers). */
 int fs_router_seeds(fs_engine* e, const fs_seed_prefix* prefixes, const int32_t* prefix_idx,

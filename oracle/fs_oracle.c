@@ -183,6 +183,145 @@ static void philox4x64_10(const uint64_t ctr_in[4], const uint64_t key_in[2], ui
 }
 
 /* ------------------------------------------------------------------------ */
+/* numpy Generator distributions used by dirichlet_skew routing             */
+/* (routing.py:99-106): rng.dirichlet(np.full(E, alpha)) then               */
+/* rng.exponential(1.0, (T, E)). Restated from numpy 2.3.5                  */
+/* (random/src/distributions/distributions.c: random_standard_exponential,  */
+/* random_standard_normal, random_standard_gamma, random_beta; and          */
+/* _generator.pyx Generator.dirichlet). The ziggurat tables are numpy's own  */
+/* (fs_ziggurat.h, extracted from libnpyrandom.a); pow/log/exp/log1p are     */
+/* glibc's, as in numpy's build, so the oracle is bit-exact by construction. */
+/* ------------------------------------------------------------------------ */
+#include "../paper_2508_03148_b200/csrc/fs_ziggurat.h"
+
+typedef struct { uint64_t key[2]; uint64_t n; uint64_t blk[4]; } np_philox;
+
+static uint64_t np_next_u64(np_philox* g) {
+  if ((g->n & 3) == 0) {
+    uint64_t ctr[4] = {g->n / 4 + 1, 0, 0, 0};
+    philox4x64_10(ctr, g->key, g->blk);
+  }
+  return g->blk[g->n++ & 3];
+}
+static double np_next_double(np_philox* g) {
+  return (double)(np_next_u64(g) >> 11) * (1.0 / 9007199254740992.0);
+}
+static double zig_d(uint64_t bits) { double d; memcpy(&d, &bits, 8); return d; }
+
+static double np_std_exponential(np_philox* g) {
+  for (;;) {
+    uint64_t ri = np_next_u64(g) >> 3;
+    uint8_t idx = (uint8_t)(ri & 0xFF);
+    ri >>= 8;
+    double x = (double)ri * zig_d(fs_zig_we[idx]);
+    if (ri < fs_zig_ke[idx]) return x;
+    if (idx == 0) return FS_ZIG_EXP_R - log1p(-np_next_double(g));
+    if ((zig_d(fs_zig_fe[idx - 1]) - zig_d(fs_zig_fe[idx])) * np_next_double(g) +
+            zig_d(fs_zig_fe[idx]) < exp(-x))
+      return x;
+  }
+}
+static double np_std_normal(np_philox* g) {
+  for (;;) {
+    uint64_t r = np_next_u64(g);
+    int idx = (int)(r & 0xff);
+    r >>= 8;
+    int sign = (int)(r & 0x1);
+    uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = (double)rabs * zig_d(fs_zig_wi[idx]);
+    if (sign & 0x1) x = -x;
+    if (rabs < fs_zig_ki[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        double xx = -FS_ZIG_NOR_INV_R * log1p(-np_next_double(g));
+        double yy = -log1p(-np_next_double(g));
+        if (yy + yy > xx * xx)
+          return ((rabs >> 8) & 0x1) ? -(FS_ZIG_NOR_R + xx) : FS_ZIG_NOR_R + xx;
+      }
+    } else {
+      if (((zig_d(fs_zig_fi[idx - 1]) - zig_d(fs_zig_fi[idx])) * np_next_double(g) +
+           zig_d(fs_zig_fi[idx])) < exp(-0.5 * x * x))
+        return x;
+    }
+  }
+}
+static double np_std_gamma(np_philox* g, double shape) {
+  if (shape == 1.0) return np_std_exponential(g);
+  if (shape == 0.0) return 0.0;
+  if (shape < 1.0) {
+    for (;;) {
+      double U = np_next_double(g);
+      double V = np_std_exponential(g);
+      if (U <= 1.0 - shape) {
+        double X = pow(U, 1. / shape);
+        if (X <= V) return X;
+      } else {
+        double Y = -log((1 - U) / shape);
+        double X = pow(1.0 - shape + shape * Y, 1. / shape);
+        if (X <= (V + Y)) return X;
+      }
+    }
+  }
+  double b = shape - 1. / 3.;
+  double c = 1. / sqrt(9 * b);
+  for (;;) {
+    double X, V;
+    do {
+      X = np_std_normal(g);
+      V = 1.0 + c * X;
+    } while (V <= 0.0);
+    V = V * V * V;
+    double U = np_next_double(g);
+    if (U < 1.0 - 0.0331 * (X * X) * (X * X)) return b * V;
+    if (log(U) < 0.5 * X * X + b * (1. - V + log(V))) return b * V;
+  }
+}
+static double np_beta(np_philox* g, double a, double b) {
+  if (a <= 1.0 && b <= 1.0) {
+    for (;;) { /* Johnk */
+      double U = np_next_double(g), V = np_next_double(g);
+      double X = pow(U, 1.0 / a), Y = pow(V, 1.0 / b);
+      double XpY = X + Y;
+      if (XpY <= 1.0 && U + V > 0.0) {
+        if (XpY > 0) return X / XpY;
+        double logX = log(U) / a, logY = log(V) / b;
+        double logM = logX > logY ? logX : logY;
+        logX -= logM;
+        logY -= logM;
+        return exp(logX - log(exp(logX) + exp(logY)));
+      }
+    }
+  }
+  double Ga = np_std_gamma(g, a), Gb = np_std_gamma(g, b);
+  return Ga / (Ga + Gb);
+}
+/* Generator.dirichlet(np.full(E, alpha)) followed by np.maximum(., 1e-12). */
+static void np_dirichlet_sym(np_philox* g, int E, double alpha, double* p) {
+  if (alpha < 0.1) { /* stick-breaking with beta variates */
+    double* csum = (double*)malloc(sizeof(double) * (size_t)E);
+    double cs = 0.0;
+    for (int j = E - 1; j >= 0; j--) { cs += alpha; csum[j] = cs; }
+    double acc = 1.0;
+    int j;
+    for (j = 0; j < E; j++) p[j] = 0.0;
+    for (j = 0; j < E - 1; j++) {
+      double v = np_beta(g, alpha, csum[j + 1]);
+      p[j] = acc * v;
+      acc *= (1. - v);
+      if (csum[j + 1] == 0) break;
+    }
+    p[E - 1] = acc;
+    free(csum);
+  } else {
+    double acc = 0.;
+    for (int j = 0; j < E; j++) { p[j] = np_std_gamma(g, alpha); acc = acc + p[j]; }
+    double invacc = 1. / acc;
+    for (int j = 0; j < E; j++) p[j] = p[j] * invacc;
+  }
+  for (int j = 0; j < E; j++) p[j] = p[j] > 1e-12 ? p[j] : 1e-12;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Python float helpers                                                     */
 /* ------------------------------------------------------------------------ */
 /* CPython 3.12 builtin sum() over a list of floats starting from int 0:
@@ -522,6 +661,54 @@ static double forest_predict(const fs_forest_set* fs, int forest, const double* 
   return mean < 1e-6 ? 1e-6 : mean;
 }
 
+/* The random part of route_tokens (routing.py:96-113) for T > 0, k < E:
+ * keys per row from rng.random (uniform) or Exp(1)/popularity (dirichlet_skew),
+ * the k smallest per row (np.argpartition(keys, k-1)[:, :k]) and their tally.
+ * An exact key tie at the selection boundary makes argpartition's pick
+ * implementation-defined: reported as FS_ERR_ROUTING_TIE. Returns a status. */
+static int route_core(int64_t T, int E, int k, int policy, double alpha, uint64_t seed,
+                      int64_t* counts) {
+  if (policy == FS_ROUTE_DIRICHLET && !(alpha > 0)) return FS_ERR_ROUTING;
+  if (policy != FS_ROUTE_UNIFORM && policy != FS_ROUTE_DIRICHLET) return FS_ERR_ROUTING;
+  np_philox g;
+  memset(&g, 0, sizeof g);
+  routing_key(seed, g.key);
+  double* pop = NULL;
+  if (policy == FS_ROUTE_DIRICHLET) {
+    pop = (double*)malloc(sizeof(double) * (size_t)E);
+    np_dirichlet_sym(&g, E, alpha, pop);
+  }
+  /* keys as order-preserving u64: rng.random() keys are (u >> 11) (the common
+   * 2^-53 scale does not change the order); dirichlet keys are positive
+   * doubles, ordered like their IEEE bit patterns */
+  uint64_t* row = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)E);
+  int st = 0;
+  for (int64_t t = 0; t < T && !st; t++) {
+    for (int e = 0; e < E; e++) {
+      if (pop) {
+        double key = np_std_exponential(&g) / pop[e];
+        memcpy(&row[e], &key, 8);
+      } else {
+        row[e] = np_next_u64(&g) >> 11;
+      }
+    }
+    for (int j = 0; j < k; j++) {
+      int best = -1;
+      for (int e = 0; e < E; e++)
+        if (row[e] != UINT64_MAX && (best < 0 || row[e] < row[best])) best = e;
+      if (j == k - 1) {
+        for (int e = 0; e < E; e++)
+          if (e != best && row[e] == row[best]) st = FS_ERR_ROUTING_TIE;
+      }
+      counts[best]++;
+      row[best] = UINT64_MAX;
+    }
+  }
+  free(row);
+  free(pop);
+  return st;
+}
+
 /* ---- route_tokens (routing.py:65-113) ---- */
 static int64_t* route(Sim* s, int64_t T, uint32_t seed, int policy_uniform_forced,
                       int rep, int mb, int64_t step, int layer) {
@@ -545,37 +732,9 @@ static int64_t* route(Sim* s, int64_t T, uint32_t seed, int policy_uniform_force
     /* zeros */
   } else if (k == E) {
     for (int e = 0; e < E; e++) counts[e] = T;
-  } else if (policy == FS_ROUTE_UNIFORM) {
-    uint64_t key[2];
-    routing_key(seed, key);
-    uint64_t* row = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)E);
-    uint64_t n = 0, blk[4] = {0, 0, 0, 0};
-    for (int64_t t = 0; t < T; t++) {
-      for (int e = 0; e < E; e++, n++) {
-        if ((n & 3) == 0) {
-          uint64_t ctr[4] = {n / 4 + 1, 0, 0, 0};
-          philox4x64_10(ctr, key, blk);
-        }
-        row[e] = blk[n & 3] >> 11; /* rng.random(): (u >> 11) * 2^-53 */
-      }
-      /* k smallest of the row: np.argpartition(keys, k-1)[:k] */
-      for (int j = 0; j < k; j++) {
-        int best = -1;
-        for (int e = 0; e < E; e++)
-          if (row[e] != UINT64_MAX && (best < 0 || row[e] < row[best])) best = e;
-        /* tie at the selection boundary: argpartition's pick is implementation-defined */
-        if (j == k - 1) {
-          for (int e = 0; e < E; e++)
-            if (e != best && row[e] == row[best]) { free(row); free(counts); fail(s, FS_ERR_ROUTING_TIE, 0); }
-        }
-        counts[best]++;
-        row[best] = UINT64_MAX;
-      }
-    }
-    free(row);
   } else {
-    free(counts);
-    fail(s, FS_ERR_UNSUPPORTED, policy);
+    int st = route_core(T, E, k, policy, d->routing_alpha, (uint64_t)seed, counts);
+    if (st) { free(counts); fail(s, st, 0); }
   }
   s->routing_calls++;
   fs_log* lg = s->log;
@@ -1505,53 +1664,34 @@ uint32_t fso_sha256_first_word(const uint8_t* msg, int64_t len) {
   return sha256_first_word(msg, (size_t)len);
 }
 void fso_routing_key(uint64_t seed, uint64_t key[2]) { routing_key(seed, key); }
-/* route_tokens(T, E, k, "uniform", seed).counts; returns status */
+/* route_tokens(T, E, k, policy, seed, alpha).counts (routing.py:65-113) for
+ * the uniform / dirichlet_skew policies; returns a status */
+int fso_route(int64_t T, int32_t E, int32_t k, int32_t policy, double alpha, uint64_t seed,
+              int32_t* counts_out) {
+  if (!(1 <= k && k <= E)) return FS_ERR_INVALID_TOPK;
+  if (T < 0) return FS_ERR_ROUTING;
+  int64_t* counts = (int64_t*)calloc((size_t)E, sizeof(int64_t));
+  int st = 0;
+  if (T == 0) {
+  } else if (k == E) {
+    for (int e = 0; e < E; e++) counts[e] = T;
+  } else {
+    st = route_core(T, E, k, policy, alpha, seed, counts);
+  }
+  for (int e = 0; e < E; e++) counts_out[e] = (int32_t)counts[e];
+  free(counts);
+  return st;
+}
 int fso_route_uniform(int64_t T, int32_t E, int32_t k, uint64_t seed, int32_t* counts_out) {
-  fs_instance_desc d;
-  memset(&d, 0, sizeof d);
-  d.num_experts = E; d.top_k = k; d.routing_policy = FS_ROUTE_UNIFORM;
-  Sim S;
-  memset(&S, 0, sizeof S);
-  S.d = &d;
-  if (setjmp(S.jb) == 0) {
-    int64_t* c = route(&S, T, (uint32_t)0, 0, 0, 0, 0, 0);
-    (void)c;
-    free(c);
-  }
-  /* route() takes the 32-bit router seed; re-run with the full seed value */
-  if (S.status) return S.status;
-  memset(&S, 0, sizeof S);
-  S.d = &d;
-  if (setjmp(S.jb) == 0) {
-    /* inline copy of route's uniform path with a 64-bit seed */
-    uint64_t key[2];
-    routing_key(seed, key);
-    int64_t* counts = (int64_t*)calloc((size_t)E, sizeof(int64_t));
-    if (T == 0) {
-    } else if (k == E) {
-      for (int e = 0; e < E; e++) counts[e] = T;
-    } else {
-      uint64_t* row = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)E);
-      uint64_t n = 0, blk[4] = {0, 0, 0, 0};
-      for (int64_t t = 0; t < T; t++) {
-        for (int e = 0; e < E; e++, n++) {
-          if ((n & 3) == 0) { uint64_t ctr[4] = {n / 4 + 1, 0, 0, 0}; philox4x64_10(ctr, key, blk); }
-          row[e] = blk[n & 3] >> 11;
-        }
-        for (int j = 0; j < k; j++) {
-          int best = -1;
-          for (int e = 0; e < E; e++)
-            if (row[e] != UINT64_MAX && (best < 0 || row[e] < row[best])) best = e;
-          counts[best]++;
-          row[best] = UINT64_MAX;
-        }
-      }
-      free(row);
-    }
-    for (int e = 0; e < E; e++) counts_out[e] = (int32_t)counts[e];
-    free(counts);
-  }
-  return S.status;
+  return fso_route(T, E, k, FS_ROUTE_UNIFORM, 0.3, seed, counts_out);
+}
+/* debugging aid for the dirichlet stream: popularity[E] and the first row of keys */
+void fso_dirichlet_row(int32_t E, double alpha, uint64_t seed, double* pop, double* keys) {
+  np_philox g;
+  memset(&g, 0, sizeof g);
+  routing_key(seed, g.key);
+  np_dirichlet_sym(&g, E, alpha, pop);
+  for (int e = 0; e < E; e++) keys[e] = np_std_exponential(&g) / pop[e];
 }
 double fso_attention_us(int decode, const int64_t* q, const int64_t* kv, int B, int hq, int hkv,
                         int hdim, double peak, double bw, double ovh, int dt) {

@@ -47,6 +47,11 @@ def load():
     lib.fso_route_uniform.restype = ctypes.c_int
     lib.fso_route_uniform.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_uint64, vp]
+    lib.fso_route.restype = ctypes.c_int
+    lib.fso_route.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                              ctypes.c_double, ctypes.c_uint64, vp]
+    lib.fso_dirichlet_row.restype = None
+    lib.fso_dirichlet_row.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, vp, vp]
     lib.fso_attention_us.restype = ctypes.c_double
     lib.fso_attention_us.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -94,6 +99,21 @@ def route_uniform(T: int, E: int, k: int, seed: int) -> tuple[list[int], int]:
     c = np.zeros(E, dtype=np.int32)
     st = load().fso_route_uniform(T, E, k, seed, abi.ptr(c))
     return c.tolist(), st
+
+
+def route(T: int, E: int, k: int, policy: str, seed: int, alpha: float = 0.3):
+    """route_tokens(T, E, k, policy, seed, alpha).counts and a status (routing.py:65-113)."""
+    c = np.zeros(E, dtype=np.int32)
+    st = load().fso_route(T, E, k, abi.ROUTING[policy], alpha, seed, abi.ptr(c))
+    return c.tolist(), st
+
+
+def dirichlet_row(E: int, alpha: float, seed: int):
+    """(popularity[E], first row of keys[E]) of route_tokens' dirichlet_skew stream."""
+    pop = np.zeros(E)
+    keys = np.zeros(E)
+    load().fso_dirichlet_row(E, alpha, seed, abi.ptr(pop), abi.ptr(keys))
+    return pop, keys
 
 
 def attention_us(decode: bool, q, kv, hq, hkv, hd, peak, bw, ovh=5.0, dt=2) -> float:

@@ -45,7 +45,7 @@ struct fs_engine {
   DevBuf descs, reps, prefixes, mid, trace, arrival, prompt, output, id_rank, order;
   // workspace
   DevBuf first, done, rank, finish, home, lists, list_base, heap, heap_base, xfer, rstate, af_ffn,
-      af_base, work, cycles, jobs, job_counts, inst_done;
+      af_base, work, cycles, jobs, job_counts, inst_done, dir_scratch;
   // outputs
   DevBuf rows, rep_out;
   // log mirrors
@@ -53,7 +53,7 @@ struct fs_engine {
       lg_members, lg_moe, lg_routes, lg_counts, lg_bcount, lg_rcount, lg_trunc;
   // cost-model scratch
   DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
-      c_layers, c_seeds, c_pf, c_mid;
+      c_layers, c_seeds, c_pf, c_mid, c_scratch;
   // learned models (persist across stages)
   DevBuf f_descs, f_roots, f_right, f_value, f_leaf;  // f_value: packed NodeP array
   fs::ForestView fv{};
@@ -273,6 +273,15 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
     P.jobs = nullptr;
     P.job_counts = nullptr;
   }
+  bool dirichlet = false;
+  for (int i = 0; i < n_instances; i++)
+    dirichlet |= descs[i].has_moe && descs[i].routing_policy == FS_ROUTE_DIRICHLET;
+  if (dirichlet) {
+    FS_CHECK(e->dir_scratch.ensure((size_t)P.n_slots * fs::kDirScratch * sizeof(double)));
+    P.dir_scratch = e->dir_scratch.as<double>();
+  } else {
+    P.dir_scratch = nullptr;
+  }
   e->n_inst = n_instances;
   e->n_reps = n_replicas;
   e->n_prefixes = n_prefixes;
@@ -463,8 +472,9 @@ int fs_attention_features(fs_engine* e, const int32_t* q_lens, const int32_t* kv
   return 0;
 }
 
-int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
-                     int32_t num_experts, int32_t top_k, int32_t* counts_out, int32_t* status) {
+int fs_route_tokens(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
+                    int32_t num_experts, int32_t top_k, int32_t policy, double alpha,
+                    int32_t* counts_out, int32_t* status) {
   if (!e) return 1;
   FS_CHECK(cudaSetDevice(e->device));
   cudaStream_t s = e->stream;
@@ -473,15 +483,27 @@ int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds,
   const size_t nc = (size_t)std::max(n_calls, 1) * std::max(num_experts, 1);
   FS_CHECK(e->c_counts.ensure(nc * 4));
   FS_CHECK(e->c_status.ensure((size_t)std::max(n_calls, 1) * 4));
-  e->last_launches = fs::launch_route_uniform(e->c_tok.as<int64_t>(), e->c_seed.as<uint64_t>(),
-                                              n_calls, num_experts, top_k,
-                                              e->c_counts.as<int32_t>(), e->c_status.as<int32_t>(), s);
+  double* scratch = nullptr;
+  if (policy == FS_ROUTE_DIRICHLET) {
+    FS_CHECK(e->c_scratch.ensure((size_t)fs::route_scratch_warps(n_calls) * fs::kDirScratch * 8));
+    scratch = e->c_scratch.as<double>();
+  }
+  e->last_launches = fs::launch_route_tokens(e->c_tok.as<int64_t>(), e->c_seed.as<uint64_t>(),
+                                             n_calls, num_experts, top_k, policy, alpha, scratch,
+                                             e->c_counts.as<int32_t>(), e->c_status.as<int32_t>(),
+                                             s);
   FS_CHECK(cudaGetLastError());
   FS_CHECK(cudaMemcpyAsync(counts_out, e->c_counts.p, 4 * (size_t)n_calls * num_experts,
                            cudaMemcpyDeviceToHost, s));
   FS_CHECK(cudaMemcpyAsync(status, e->c_status.p, 4 * (size_t)n_calls, cudaMemcpyDeviceToHost, s));
   FS_CHECK(cudaStreamSynchronize(s));
   return 0;
+}
+
+int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
+                     int32_t num_experts, int32_t top_k, int32_t* counts_out, int32_t* status) {
+  return fs_route_tokens(e, tokens, seeds, n_calls, num_experts, top_k, FS_ROUTE_UNIFORM, 0.3,
+                         counts_out, status);
 }
 
 int fs_set_forests(fs_engine* e, fs_forest_set f) {

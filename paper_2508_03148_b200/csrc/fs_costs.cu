@@ -17,6 +17,7 @@
 #include "fs_device.cuh"
 #include "fs_engine.h"
 #include "fs_route.cuh"
+#include "fs_dirichlet.cuh"
 
 namespace fs {
 
@@ -368,20 +369,30 @@ int launch_attention_features(const int32_t* q, const int32_t* kv, const int64_t
 }
 
 // ---- routing / seeds (for parity tests and the routing benchmark) -----------------------------
+constexpr int kRouteWarpsPerCta = 4;
+constexpr int kRouteMaxCtas = 148 * 8;
+
 __global__ void route_kernel(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
-                             int32_t* counts, int32_t* status) {
-  __shared__ int sm_counts[4][FS_MAX_EXPERTS];
+                             int policy, double alpha, double* scratch, int32_t* counts,
+                             int32_t* status) {
+  __shared__ int sm_counts[kRouteWarpsPerCta][FS_MAX_EXPERTS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int c = blockIdx.x * 4 + w; c < n; c += gridDim.x * 4) {
+  const int gw = blockIdx.x * kRouteWarpsPerCta + w;
+  for (int c = gw; c < n; c += gridDim.x * kRouteWarpsPerCta) {
     int st;
     const int64_t T = tokens[c];
     if (!(1 <= k && k <= E)) st = FS_ERR_INVALID_TOPK;
     else if (E > FS_MAX_EXPERTS || (k < E && k > FS_MAX_TOPK)) st = FS_ERR_CAPACITY;
     else if (T < 0) st = FS_ERR_ROUTING;
+    else if (policy != FS_ROUTE_UNIFORM && policy != FS_ROUTE_DIRICHLET) st = FS_ERR_ROUTING;
     else {
       uint64_t key[2] = {0, 0};
       routing_key(seeds[c], key);
-      st = route_uniform_warp(lane, T, E, k, key[0], key[1], sm_counts[w]);
+      if (policy == FS_ROUTE_DIRICHLET && T > 0 && k < E)
+        st = route_dirichlet_warp(lane, T, E, k, alpha, key[0], key[1],
+                                  scratch + (int64_t)gw * kDirScratch, sm_counts[w]);
+      else
+        st = route_uniform_warp(lane, T, E, k, key[0], key[1], sm_counts[w]);
     }
     __syncwarp();
     for (int e = lane; e < E; e += 32)
@@ -391,12 +402,19 @@ __global__ void route_kernel(const int64_t* tokens, const uint64_t* seeds, int n
   }
 }
 
-int launch_route_uniform(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
-                         int32_t* counts, int32_t* status, void* stream) {
+int route_scratch_warps(int n) {
+  int blocks = (n + kRouteWarpsPerCta - 1) / kRouteWarpsPerCta;
+  if (blocks > kRouteMaxCtas) blocks = kRouteMaxCtas;
+  return (blocks < 1 ? 1 : blocks) * kRouteWarpsPerCta;
+}
+
+int launch_route_tokens(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
+                        int policy, double alpha, double* scratch, int32_t* counts,
+                        int32_t* status, void* stream) {
   if (n <= 0) return 0;
-  int blocks = (n + 3) / 4;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  route_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(tokens, seeds, n, E, k, counts, status);
+  const int blocks = route_scratch_warps(n) / kRouteWarpsPerCta;
+  route_kernel<<<blocks, 32 * kRouteWarpsPerCta, 0, (cudaStream_t)stream>>>(
+      tokens, seeds, n, E, k, policy, alpha, scratch, counts, status);
   return 1;
 }
 

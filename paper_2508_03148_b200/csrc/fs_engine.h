@@ -34,6 +34,9 @@ struct RepState {
 };
 
 constexpr int kJobLayers = 32;  // layers routed per job
+// dirichlet_skew router scratch per warp (fs_dirichlet.cuh): popularity[E] + a key ring
+constexpr int kDirRing = 2048;  // keys of unfinished rows + one window (>= 1023 + 128)
+constexpr int kDirScratch = FS_MAX_EXPERTS + kDirRing;  // doubles
 
 // A routing job: the uniform router calls of up to kJobLayers layers of one
 // batch (routing.py:65-113, one call per layer), split into chunks of rows
@@ -89,6 +92,7 @@ struct EngineParams {
   int32_t job_max_e;
   int32_t* inst_done;            // instances finished (helpers stop at n_inst)
   int32_t* open_jobs;            // published jobs with unclaimed chunks
+  double* dir_scratch;           // [n_slots][kDirScratch]: dirichlet_skew popularity + key ring
   ForestView fv;                 // learned operator models (fs_set_forests)
 };
 
@@ -115,8 +119,10 @@ int launch_attention_features(const int32_t* q, const int32_t* kv, const int64_t
 int launch_attention_forest(const ForestView& fv, int forest, const int32_t* q, const int32_t* kv,
                             const int64_t* off, const uint8_t* dec, int64_t nb, fs_attn_params prm,
                             double* out, int n_sms, void* stream);
-int launch_route_uniform(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
-                         int32_t* counts, int32_t* status, void* stream);
+int launch_route_tokens(const int64_t* tokens, const uint64_t* seeds, int n, int E, int k,
+                        int policy, double alpha, double* scratch, int32_t* counts,
+                        int32_t* status, void* stream);
+int route_scratch_warps(int n);  // warps (scratch slots) launch_route_tokens uses for n calls
 int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int32_t* pidx,
                         const int32_t* mb, const int64_t* steps, const int32_t* layers, int n,
                         uint32_t* out, void* stream);

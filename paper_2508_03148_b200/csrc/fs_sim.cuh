@@ -40,6 +40,7 @@
 #include "fs_device.cuh"
 #include "fs_engine.h"
 #include "fs_route.cuh"
+#include "fs_dirichlet.cuh"
 
 namespace fs {
 namespace FS_SIM_NS {
@@ -257,7 +258,10 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
     __syncwarp();
     return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
   }
-  return FS_ERR_UNSUPPORTED;  // dirichlet_skew is not on the device path yet
+  if (policy == FS_ROUTE_DIRICHLET)
+    return route_dirichlet_warp(I.lane, T, E, k, d->routing_alpha, k0, k1,
+                                P.dir_scratch + (int64_t)I.slot * kDirScratch, sm->counts);
+  return FS_ERR_ROUTING;
 }
 
 __device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,

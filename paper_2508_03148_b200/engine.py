@@ -57,6 +57,8 @@ def load_library(path: str = LIB_PATH):
         "fs_attention_features": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp]),
         "fs_attention_features_dev": (ctypes.c_int, [vp, vp, vp, vp, vp, i64, _AttnParamsC, vp, vp]),
         "fs_route_uniform": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
+        "fs_route_tokens": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, i32, ctypes.c_double, vp,
+                                           vp]),
         "fs_router_seeds": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i32, vp]),
         "fs_set_forests": (ctypes.c_int, [vp, abi.ForestSetC]),
         "fs_attention_forest": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i64, _AttnParamsC, vp]),
@@ -340,6 +342,20 @@ class Engine:
         self._check(self.lib.fs_route_uniform(self.h, abi.ptr(tokens), abi.ptr(seeds), n,
                                               num_experts, top_k, abi.ptr(counts), abi.ptr(st)),
                     "fs_route_uniform")
+        return counts[:n], st[:n]
+
+    def route_tokens(self, tokens, seeds, num_experts: int, top_k: int, policy: str = "uniform",
+                     alpha: float = 0.3):
+        """route_tokens(T, E, k, policy, seed, alpha).counts per call (routing.py:65-113)
+        for the uniform and dirichlet_skew policies; returns (counts, status)."""
+        tokens = np.ascontiguousarray(tokens, dtype=np.int64)
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        n = len(tokens)
+        counts = np.zeros((max(n, 1), num_experts), dtype=np.int32)
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        self._check(self.lib.fs_route_tokens(self.h, abi.ptr(tokens), abi.ptr(seeds), n,
+                                             num_experts, top_k, abi.ROUTING[policy], alpha,
+                                             abi.ptr(counts), abi.ptr(st)), "fs_route_tokens")
         return counts[:n], st[:n]
 
     def router_seeds(self, prefixes: list[str], prefix_idx, micro_batch, steps, layers):

@@ -485,6 +485,57 @@ def learned_scenarios() -> dict[str, dict]:
     return s
 
 
+def dirichlet_fixtures() -> dict:
+    """dirichlet_skew routing (routing.py:99-106): route_tokens counts from the
+    reference, the raw stream (popularity + first key row) from the reference's
+    own _rng, and whole simulations that route with the policy."""
+    from frontier_sim.costmodel.routing import _rng, route_tokens
+
+    out: dict = {}
+    routes = []
+    cases = [(1, 8, 2), (37, 8, 2), (300, 8, 2), (5, 256, 8), (40, 256, 8), (100, 64, 6),
+             (20, 16, 3), (9, 60, 6), (3, 1024, 16), (64, 8, 7), (0, 8, 2), (12, 4, 4)]
+    for T, E, k in cases:
+        for alpha in (0.3, 0.05, 1.0, 2.5):
+            for seed in (0, 1, 3735928559, 2**32 - 1):
+                try:
+                    c = list(route_tokens(T, E, k, "dirichlet_skew", seed, alpha).counts)
+                except Exception as exc:  # pragma: no cover - none expected
+                    c = f"{type(exc).__name__}: {exc}"
+                routes.append([T, E, k, alpha, seed, c])
+    out["route_dirichlet"] = routes
+    streams = []
+    for E in (8, 64, 256):
+        for alpha in (0.3, 0.05, 2.5):
+            for seed in (0, 7, 123456789):
+                g = _rng(seed)
+                pop = np.maximum(g.dirichlet(np.full(E, alpha)), 1e-12)
+                keys = g.exponential(1.0, (2, E)) / pop
+                streams.append([E, alpha, seed, [int(x) for x in pop.view(np.uint64)],
+                                [int(x) for x in keys[0].view(np.uint64)]])
+    out["dirichlet_stream"] = streams
+    sims = {}
+    d = copy.deepcopy(W.c5_sweep_configs(24)[48 + 5])  # Mixtral ep=2
+    d["seed"] = 21
+    d["routing"] = {"policy": "dirichlet_skew", "alpha": 0.3}
+    sims["co_mixtral_dirichlet"] = d
+    d = copy.deepcopy(W.c5_sweep_configs(16)[48 + 2])
+    d["seed"] = 22
+    d["routing"] = {"policy": "dirichlet_skew", "alpha": 0.05}
+    sims["co_mixtral_dirichlet_small_alpha"] = d
+    d = W.c4_colocated_ep(6, seed=23)
+    d["routing"] = {"policy": "dirichlet_skew", "alpha": 0.3}
+    sims["co_dsv3_ep8_dirichlet"] = d
+    d = W.c4_af(6, seed=24)
+    d["routing"] = {"policy": "dirichlet_skew", "alpha": 2.0}
+    sims["af_dsv3_dirichlet"] = d
+    out["scenarios"] = {name: record(doc, with_batches=True, with_routes=True)
+                        for name, doc in sims.items()}
+    for name, r in out["scenarios"].items():
+        print(name, r.get("iterations"), r.get("error"), f"{r['wall_s']:.2f}s")
+    return out
+
+
 def write(name: str, payload) -> None:
     payload = {"numpy": np.__version__, "python": sys.version.split()[0], "data": payload}
     path = os.path.join(HERE, f"{name}.json.gz")
@@ -511,6 +562,8 @@ def main() -> None:
             print(name, sc[name].get("iterations"), sc[name].get("error"),
                   f"{sc[name]['wall_s']:.2f}s")
         write("scenarios", sc)
+    if only is None or "dirichlet" in only:
+        write("dirichlet", dirichlet_fixtures())
     if only is None or "forest" in only:
         write("forest_predictions", forest_fixtures())
         sc = {}
