@@ -754,6 +754,55 @@ static int64_t* route(Sim* s, int64_t T, uint32_t seed, int policy_uniform_force
   return counts;
 }
 
+/* GroupedGemmFeatures(total, counts, d_model, d_ff, top_k, "local").vector()
+ * (features.py:126-209) for one EP rank's expert loads: numpy mean / std
+ * (pairwise sums, _var's (x - mean)^2), active-expert mean, normalised entropy
+ * -(p * log p).sum() / log(n). log is glibc's here; numpy's np.log may use its
+ * own SIMD kernel (SVML on AVX-512 hosts), which can differ in the last bit --
+ * the features only feed `x[f] <= threshold` comparisons. */
+static void gg_local_features(const int64_t* counts, int n, int64_t d_model, int64_t d_ff,
+                              int top_k, double x[12]) {
+  double* a = (double*)malloc(sizeof(double) * (size_t)n);
+  double* w = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t total = 0, nact = 0, mx = counts[0];
+  for (int i = 0; i < n; i++) {
+    a[i] = (double)counts[i];
+    total += counts[i];
+    nact += counts[i] > 0;
+    if (counts[i] > mx) mx = counts[i];
+  }
+  const double sum = np_pairwise(a, n);           /* exact: integer values */
+  const double mean = sum / (double)n;
+  for (int i = 0; i < n; i++) { double dv = a[i] - mean; w[i] = dv * dv; }
+  const double std = sqrt(np_pairwise(w, n) / (double)n);
+  const double sel = (double)nact / (double)n;
+  double mom = 0.0;
+  if (nact) {
+    int j = 0;
+    for (int i = 0; i < n; i++) if (counts[i] > 0) w[j++] = a[i];
+    const double amean = np_pairwise(w, nact) / (double)nact;
+    mom = (double)mx / amean;
+  }
+  const double cv = mean > 0 ? std / mean : 0.0;
+  double ent;
+  if (n == 1) {
+    ent = 1.0;
+  } else if (sum > 0) {
+    int j = 0;
+    for (int i = 0; i < n; i++) {
+      if (counts[i] > 0) { double pr = a[i] / sum; w[j++] = pr * log(pr); }
+    }
+    ent = -np_pairwise(w, nact) / log((double)n);
+  } else {
+    ent = 0.0;
+  }
+  x[0] = (double)total; x[1] = (double)n; x[2] = (double)d_model; x[3] = (double)d_ff;
+  x[4] = (double)top_k; x[5] = sel; x[6] = mom; x[7] = cv; x[8] = ent;
+  x[9] = (double)mx; x[10] = mean; x[11] = std;
+  free(a);
+  free(w);
+}
+
 /* moe_layer_latency (moe.py:69-128); returns total; *ratio gets the
  * moe_imbalance raw value (base.py:247-252) */
 static double moe_layer(Sim* s, const int64_t* counts, int64_t T, const fs_cost_ctx* c,
@@ -778,7 +827,19 @@ static double moe_layer(Sim* s, const int64_t* counts, int64_t T, const fs_cost_
     int64_t local = 0;
     for (int e = 0; e < per; e++) local += counts[r * per + e];
     double v = 0.0;
-    if (local != 0) v = grouped_gemm_us(s, counts + r * per, per, d->d_model, dffs, d->ffn_matrices, c, d->dtype_bytes);
+    if (local != 0) {
+      if (d->gg_forest != -1) {
+        /* CostModel.predict_grouped_gemm with a learned model (model.py:323-326) */
+        if (d->gg_forest < 0) fail(s, FS_ERR_SCHEMA, 0);
+        if (!s->forests || d->gg_forest >= s->forests->n_forests) fail(s, FS_ERR_INTERNAL, 7);
+        if (dffs < 1 || d->top_k < 1) fail(s, FS_ERR_VALUE, 3);
+        double x[12];
+        gg_local_features(counts + r * per, per, d->d_model, dffs, d->top_k, x);
+        v = forest_predict(s->forests, d->gg_forest, x);
+      } else {
+        v = grouped_gemm_us(s, counts + r * per, per, d->d_model, dffs, d->ffn_matrices, c, d->dtype_bytes);
+      }
+    }
     if (r == 0 || v > expert) expert = v; /* max(): first maximum */
     pysum_add(&ps, v);
   }
@@ -1445,7 +1506,6 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
 
   if (setjmp(s->jb) == 0) {
     /* learned grouped GEMM on MoE layers needs numpy's np.log (entropy): next */
-    if (d->has_moe && d->gg_forest != -1) fail(s, FS_ERR_UNSUPPORTED, 101);
     /* schedule_arrivals (base.py:167-177): seq 0..N-1 */
     for (int i = 0; i < N; i++) schedule(s, arrival[i], EV_ARRIVAL, -1, i);
     while (s->hn) {
@@ -1684,6 +1744,13 @@ int fso_route(int64_t T, int32_t E, int32_t k, int32_t policy, double alpha, uin
 }
 int fso_route_uniform(int64_t T, int32_t E, int32_t k, uint64_t seed, int32_t* counts_out) {
   return fso_route(T, E, k, FS_ROUTE_UNIFORM, 0.3, seed, counts_out);
+}
+/* GroupedGemmFeatures(..., mode="local").vector() and, with a forest set, the
+ * learned prediction (features.py:166-209, model.py:323-326) */
+double fso_gg_features(const fs_forest_set* fs, int forest, const int64_t* counts, int n,
+                       int64_t d_model, int64_t d_ff, int top_k, double* x12) {
+  gg_local_features(counts, n, d_model, d_ff, top_k, x12);
+  return fs ? forest_predict(fs, forest, x12) : 0.0;
 }
 /* debugging aid for the dirichlet stream: popularity[E] and the first row of keys */
 void fso_dirichlet_row(int32_t E, double alpha, uint64_t seed, double* pop, double* keys) {

@@ -52,6 +52,9 @@ def load():
                               ctypes.c_double, ctypes.c_uint64, vp]
     lib.fso_dirichlet_row.restype = None
     lib.fso_dirichlet_row.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, vp, vp]
+    lib.fso_gg_features.restype = ctypes.c_double
+    lib.fso_gg_features.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int, vp]
     lib.fso_attention_us.restype = ctypes.c_double
     lib.fso_attention_us.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -133,6 +136,16 @@ def attention_forest(forests, forest: int, decode: bool, q, kv, hq: int, hkv: in
     v = load().fso_attention_forest(ctypes.byref(fset), forest, int(decode), abi.ptr(q),
                                     abi.ptr(kv), len(q), hq, hkv, hd, abi.ptr(x))
     return v, x
+
+
+def gg_features(counts, d_model: int, d_ff: int, top_k: int, forests=None, forest: int = 0):
+    """(GroupedGemmFeatures(..., "local").vector(), learned prediction or 0.0)."""
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    x = np.zeros(12)
+    fset = forest_set_struct(forests) if forests is not None else None
+    v = load().fso_gg_features(ctypes.byref(fset) if fset is not None else None, forest,
+                               abi.ptr(c), len(c), d_model, d_ff, top_k, abi.ptr(x))
+    return x, v
 
 
 def pysum(xs) -> float:

@@ -254,6 +254,8 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
       }
       if (f != -1) e->learned = true;
     }
+    // dirichlet_skew routing is compiled into the extended (learned) kernel variant only
+    if (descs[i].has_moe && descs[i].routing_policy == FS_ROUTE_DIRICHLET) e->learned = true;
   }
   P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned);
   int max_e = 0;
@@ -275,7 +277,8 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   }
   bool dirichlet = false;
   for (int i = 0; i < n_instances; i++)
-    dirichlet |= descs[i].has_moe && descs[i].routing_policy == FS_ROUTE_DIRICHLET;
+    dirichlet |= descs[i].has_moe && (descs[i].routing_policy == FS_ROUTE_DIRICHLET ||
+                                      descs[i].gg_forest != -1);  // learned MoE: entropy scratch
   if (dirichlet) {
     FS_CHECK(e->dir_scratch.ensure((size_t)P.n_slots * fs::kDirScratch * sizeof(double)));
     P.dir_scratch = e->dir_scratch.as<double>();

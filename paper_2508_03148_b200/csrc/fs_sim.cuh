@@ -42,6 +42,14 @@
 #include "fs_route.cuh"
 #include "fs_dirichlet.cuh"
 
+// compile-time knobs (scripts/variants.py builds and times alternatives)
+#ifndef FS_PHILOX_ILP  // Philox blocks per lane in flight in the routing pass (1 measured best)
+#define FS_PHILOX_ILP 1
+#endif
+#ifndef FS_DIR_IN_ANALYTIC
+#define FS_DIR_IN_ANALYTIC 0
+#endif
+
 namespace fs {
 namespace FS_SIM_NS {
 
@@ -258,10 +266,14 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
     __syncwarp();
     return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
   }
+#if FS_LEARNED || FS_DIR_IN_ANALYTIC
+  // dirichlet_skew instances run in the extended (learned) variant of this kernel:
+  // the call would cost the analytic variant's register allocation
   if (policy == FS_ROUTE_DIRICHLET)
     return route_dirichlet_warp(I.lane, T, E, k, d->routing_alpha, k0, k1,
                                 P.dir_scratch + (int64_t)I.slot * kDirScratch, sm->counts);
-  return FS_ERR_ROUTING;
+#endif
+  return policy == FS_ROUTE_DIRICHLET ? FS_ERR_INTERNAL : FS_ERR_ROUTING;
 }
 
 __device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
@@ -299,6 +311,10 @@ __device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t
 constexpr unsigned kChunkBits = 20;
 constexpr unsigned long long kChunkMask = (1ull << kChunkBits) - 1;
 constexpr int kMaxChunks = 1 << 18;
+#ifndef FS_CHUNK_BLOCKS  // Philox blocks per lane per claimed chunk
+#define FS_CHUNK_BLOCKS 48
+#endif
+constexpr int kChunkBlocks = FS_CHUNK_BLOCKS;
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
@@ -307,15 +323,33 @@ __device__ __forceinline__ int ld_volatile_i32(const int32_t* p) {
   return *reinterpret_cast<const volatile int32_t*>(p);
 }
 
-// returns a claimed chunk index or -1 (same on all lanes). A successful claim is
-// followed by a fence so the job parameters, written before the job was
-// published, are visible; the claimant of the last chunk closes the job.
+// acquire / release atomics (cheaper than a full __threadfence per chunk)
+__device__ __forceinline__ unsigned long long atom_add_acquire_u64(unsigned long long* p,
+                                                                   unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acquire.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release_i32(int32_t* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_i32(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// returns a claimed chunk index or -1 (same on all lanes). The claim is an
+// acquire (the job parameters were written before the job was published with a
+// release), passed on to the other lanes by __syncwarp; the claimant of the
+// last chunk closes the job.
 __device__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
   long long c = -1;
   if (lane == 0) {
     const unsigned long long v = ld_volatile_u64(&job->ctr);
     if ((v & kChunkMask) < ((v >> kChunkBits) & kChunkMask)) {
-      const unsigned long long old = atomicAdd(&job->ctr, 1ull);
+      const unsigned long long old = atom_add_acquire_u64(&job->ctr, 1ull);
       const unsigned long long n = (old >> kChunkBits) & kChunkMask;
       if ((old & kChunkMask) < n) {
         c = (long long)(old & kChunkMask);
@@ -323,8 +357,8 @@ __device__ int claim_chunk(const EngineParams& P, RouteJob* job, int lane) {
       }
     }
   }
+  __syncwarp();
   c = __shfl_sync(FS_FULL, c, 0);
-  if (c >= 0) __threadfence();
   return (int)c;
 }
 
@@ -342,8 +376,7 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
   uint32_t thr = 0xFFFFFFFFu;
   if (!active || e0 >= e1) return;
   const uint64_t n0 = rb + e0, n1 = rb + e1;
-  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) {
-    const U4 blk = philox4x64_10(b + 1, k0, k1);
+  auto consume = [&](const U4& blk, uint64_t b) {
     const uint64_t base = 4 * b;
     const int jlo = n0 > base ? (int)(n0 - base) : 0;
     const int jhi = (n1 - base) < 4 ? (int)(n1 - base) : 4;
@@ -367,12 +400,24 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
         }
       }
     }
+  };
+#if FS_PHILOX_ILP >= 2
+  // two blocks per step (a trailing odd block is generated and ignored)
+  const uint64_t blast = (n1 - 1) >> 2;
+  for (uint64_t b = n0 >> 2; b <= blast; b += 2) {
+    U4 A, B;
+    philox4x64_10_x2(b + 1, b + 2, k0, k1, A, B);
+    consume(A, b);
+    if (b + 1 <= blast) consume(B, b + 1);
   }
+#else
+  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) consume(philox4x64_10(b + 1, k0, k1), b);
+#endif
 }
 
 template <int KCAP>
 __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
-                                int lane) {
+                                int lane, int* tally) {
   const int64_t T = __ldcg(&job->T);
   const int E = __ldcg(&job->E), k = __ldcg(&job->k), nl = __ldcg(&job->nl);
   const int nseg = __ldcg(&job->nseg), ppc = __ldcg(&job->passes_per_chunk);
@@ -393,6 +438,16 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
   int64_t r = row_j - (int64_t)layer * T;
   int key_layer = -1;
   uint64_t k0 = 0, k1 = 0;
+  // the chunk's tally goes to the warp's shared-memory histogram when the
+  // layers it spans fit (flushed once at the end), else straight to global
+  const int64_t row_end = min(total_rows, row0 + (int64_t)ppc * rpp);
+  const int l_first = (int)(row0 / T);
+  const int span = row_end > row0 ? (int)((row_end - 1) / T) - l_first + 1 : 0;
+  const bool local = span * E <= FS_MAX_EXPERTS;
+  if (local) {
+    for (int i = lane; i < span * E; i += 32) tally[i] = 0;
+    __syncwarp();
+  }
   for (int p = 0; p < ppc; p++) {
     if (row0 + (int64_t)p * rpp >= total_rows) break;
     const bool active = row_j < total_rows;
@@ -448,30 +503,70 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
         if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
       }
     }
+    if (local) {
+      if (leader) {
 #pragma unroll
-    for (int j = 0; j < KCAP; j++) {
-      if (j < k) {
-        const int key = leader ? layer * E + ids[j] : -1;
-        const unsigned grp = __match_any_sync(FS_FULL, key);
-        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counts[key], __popc(grp));
+        for (int j = 0; j < KCAP; j++)
+          if (j < k) atomicAdd(&tally[(layer - l_first) * E + ids[j]], 1);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < KCAP; j++) {
+        if (j < k) {
+          const int key = leader ? layer * E + ids[j] : -1;
+          const unsigned grp = __match_any_sync(FS_FULL, key);
+          if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counts[key], __popc(grp));
+        }
       }
     }
     r += rpp;
     row_j += rpp;
     while (r >= T) { r -= T; layer++; }
   }
+  if (local) {
+    __syncwarp();
+    for (int i = lane; i < span * E; i += 32) {
+      const int v = tally[i];
+      if (v) atomicAdd(&counts[l_first * E + i], v);
+    }
+    __syncwarp();
+  }
   if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
 }
 
+// publish: completion is a release by lane 0 after __syncwarp (orders every
+// lane's tally atomics before it); private jobs (run by their owner alone)
+// skip it
 __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
-                              int lane) {
+                              int lane, int* tally, bool publish) {
   const int k = __ldcg(&job->k);
-  if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane);
-  else if (k + 1 <= 9) process_chunk_k<9>(P, job, counts, c, lane);
-  else process_chunk_k<FS_MAX_TOPK + 1>(P, job, counts, c, lane);
-  __threadfence();
-  if (lane == 0) atomicAdd(&job->done, 1);
+  if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane, tally);
+  else if (k + 1 <= 9) process_chunk_k<9>(P, job, counts, c, lane, tally);
+  else process_chunk_k<FS_MAX_TOPK + 1>(P, job, counts, c, lane, tally);
   __syncwarp();
+  if (publish && lane == 0) red_add_release_i32(&job->done, 1);
+}
+
+// Chunk loops. With FS_JOB_NOINLINE they are out-of-line calls: the caller's
+// instance state is saved once per job around the call, and the routing loop
+// inside gets the register file to itself (one copy of the code for owners and
+// helpers alike).
+#ifndef FS_JOB_NOINLINE  // 0 measured best (313 vs 340 ms for the C5 sweep)
+#define FS_JOB_NOINLINE 0
+#endif
+#if FS_JOB_NOINLINE
+#define FS_JOB_FN __device__ __noinline__
+#else
+#define FS_JOB_FN __device__ __forceinline__
+#endif
+FS_JOB_FN void drain_job(const EngineParams& P, RouteJob* job, int32_t* counts, int lane,
+                         int* tally) {
+  for (int c; (c = claim_chunk(P, job, lane)) >= 0;)
+    process_chunk(P, job, counts, c, lane, tally, true);
+}
+FS_JOB_FN void run_chunks(const EngineParams& P, RouteJob* job, int32_t* counts, int n, int lane,
+                          int* tally) {
+  for (int c = 0; c < n; c++) process_chunk(P, job, counts, c, lane, tally, false);
 }
 
 __device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slot) {
@@ -481,7 +576,7 @@ __device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slo
 // Route layers [l0, l0+nl) of one batch; the tally of layer l0+j ends up at
 // job_counts_of(slot)[j*E ...]. Returns FS_OK or FS_ERR_ROUTING_TIE.
 __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
-                             int l0, int nl, int64_t T) {
+                             int l0, int nl, int64_t T, int* tally) {
   const fs_instance_desc* d = I.d;
   RouteJob* job = &P.jobs[I.slot];
   int32_t* counts = job_counts_of(P, I.slot);
@@ -511,7 +606,7 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
   const int rpp = 32 / nseg;
   const int64_t passes = (rows + rpp - 1) / rpp;
   const int blocks_per_pass = ((E + nseg - 1) / nseg + 3) / 4 + 1;
-  int ppc = 16 / blocks_per_pass;
+  int ppc = kChunkBlocks / blocks_per_pass;
   if (ppc < 1) ppc = 1;
   int64_t n_chunks = (passes + ppc - 1) / ppc;
   if (n_chunks > kMaxChunks) {
@@ -536,10 +631,10 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
   }
   __syncwarp();
   if (shared) {
-    for (int c; (c = claim_chunk(P, job, I.lane)) >= 0;) process_chunk(P, job, counts, c, I.lane);
-    while (ld_volatile_i32(&job->done) < n_chunks) __nanosleep(64);
+    drain_job(P, job, counts, I.lane, tally);
+    while (ld_acquire_i32(&job->done) < n_chunks) __nanosleep(64);
   } else {
-    for (int c = 0; c < n_chunks; c++) process_chunk(P, job, counts, c, I.lane);
+    run_chunks(P, job, counts, (int)n_chunks, I.lane, tally);
   }
   __threadfence();
   __syncwarp();
@@ -549,6 +644,9 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
 // uniform routing with real draws goes through the job board; the trace policy
 // and the RNG-free shortcuts (T == 0, top_k == E) stay on the owning warp
 __device__ __forceinline__ bool use_job_board(const fs_instance_desc* d, int policy, int64_t T) {
+#if FS_LEARNED
+  if (d->gg_forest != -1) return false;  // learned MoE layers cost per layer from sm->counts
+#endif
   return policy == FS_ROUTE_UNIFORM && T > 0 && d->top_k < d->num_experts &&
          d->top_k >= 1 && d->top_k <= FS_MAX_TOPK && d->num_experts <= FS_MAX_EXPERTS;
 }
@@ -564,7 +662,7 @@ __device__ void load_job_layer(const EngineParams& P, const Inst& I, int j, Warp
 
 // warps with no instance left help route other warps' jobs until every
 // instance has finished; they sleep (exponential backoff) while no job is open
-__device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
+__device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot, int* tally) {
   const int ns = P.n_slots;
   const int start = (int)(((unsigned)my_slot * 37u) % (unsigned)ns);
   unsigned backoff = 32;
@@ -589,8 +687,7 @@ __device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot) {
         m &= m - 1;
         const int sp = __shfl_sync(FS_FULL, s, pick);
         RouteJob* job = &P.jobs[sp];
-        for (int c; (c = claim_chunk(P, job, lane)) >= 0;)
-          process_chunk(P, job, job_counts_of(P, sp), c, lane);
+        drain_job(P, job, job_counts_of(P, sp), lane, tally);
       }
     }
   }
@@ -672,6 +769,100 @@ __device__ __noinline__ double learned_dense_ffn_us(const EngineParams& P, Inst&
 }
 #define FFN_DENSE_US(c, n) \
   (d->gg_forest != -1 ? learned_dense_ffn_us(P, I, (c), (n), sm) : dense_ffn_us(d, (c), (n)))
+
+// moe_layer_latency (moe.py:69-128) with a learned grouped-GEMM model: per EP
+// rank with tokens, GroupedGemmFeatures(local, counts, d_model, d_ff_shard,
+// top_k, "local").vector() (features.py:166-209) then the forest
+// (model.py:323-326). Counts are the layer's tally in sm->counts. Sums of the
+// integer loads are exact in any order; the std and the entropy sum follow
+// numpy's pairwise order (the entropy terms p * log(p) of the active experts are
+// compacted into the warp's global scratch first). Same outputs as
+// moe_layer_warp; status uniform across lanes.
+__device__ __noinline__ int learned_moe_layer_warp(const EngineParams& P, Inst& I, WarpSmem* sm,
+                                                   int64_t T, int ep, int moe_tp,
+                                                   const fs_cost_ctx& c, double* total,
+                                                   double* ratio) {
+  const fs_instance_desc* d = I.d;
+  const int E = d->num_experts, lane = I.lane;
+  if (ep < 1 || moe_tp < 1 || E % ep != 0 || d->expert_d_ff % moe_tp != 0)
+    return FS_ERR_TOPOLOGY_MISMATCH;
+  if (T < 1) return FS_ERR_EMPTY_BATCH;
+  if (d->gg_forest < 0) return FS_ERR_SCHEMA;  // check_schema("grouped_gemm_v1")
+  const double gate = linear_us(T, E, d->d_model, c, d->dtype_bytes);
+  const int64_t routed_bytes = T * (int64_t)d->top_k * d->d_model * d->dtype_bytes;
+  const double dispatch = collective_flt(false, i2d(routed_bytes) / (double)ep, ep,
+                                         d->intra_latency_s, d->intra_bandwidth_bps) * 1e6;
+  const int per = E / ep;
+  const int64_t dffs = d->expert_d_ff / moe_tp;
+  double* plogp = P.dir_scratch + (int64_t)I.slot * kDirScratch;
+  double best = -1.0;
+  PySum ps;
+  ps.init();
+  for (int r = 0; r < ep; r++) {
+    const int* cr = sm->counts + r * per;
+    int64_t loc = 0, mx = INT64_MIN, nact = 0;
+    for (int e = lane; e < per; e += 32) {
+      const int64_t v = cr[e];
+      loc += v;
+      mx = v > mx ? v : mx;
+      nact += v > 0;
+    }
+    loc = warp_sum_i64(loc);
+    mx = warp_max_i64(mx);
+    nact = warp_sum_i64(nact);
+    double v = 0.0;
+    if (loc != 0) {
+      if (dffs < 1 || d->top_k < 1) return FS_ERR_VALUE;
+      const double sum = i2d(loc);
+      const double mean = sum / (double)per;
+      auto dev2 = [&](int64_t i) { const double dv = (double)cr[i] - mean; return dv * dv; };
+      const double stdv = sqrt(np_pairwise_w(0, per, dev2, lane) / (double)per);
+      const double amean = sum / (double)nact;  // active.mean(): exact integer sum
+      double ent;
+      if (per == 1) {
+        ent = 1.0;
+      } else {
+        __syncwarp();
+        int base = 0;  // active experts before this chunk (compaction keeps index order)
+        for (int e0 = 0; e0 < per; e0 += 32) {
+          const int e = e0 + lane;
+          const bool act = e < per && cr[e] > 0;
+          const unsigned m = __ballot_sync(FS_FULL, act);
+          if (act) {
+            const double pr = (double)cr[e] / sum;
+            plogp[base + __popc(m & ((1u << lane) - 1u))] = pr * log(pr);
+          }
+          base += __popc(m);
+        }
+        __syncwarp();
+        auto term = [&](int64_t i) { return plogp[i]; };
+        ent = -np_pairwise_w(0, nact, term, lane) / log((double)per);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        double* x = sm->fx;
+        x[0] = sum; x[1] = (double)per; x[2] = (double)d->d_model; x[3] = (double)dffs;
+        x[4] = (double)d->top_k; x[5] = (double)nact / (double)per;
+        x[6] = (double)mx / amean; x[7] = mean > 0 ? stdv / mean : 0.0; x[8] = ent;
+        x[9] = (double)mx; x[10] = mean; x[11] = stdv;
+      }
+      __syncwarp();
+      v = forest_predict_w(P.fv, d->gg_forest, sm->fx, sm->fvals, lane);
+      __syncwarp();
+    }
+    if (v > best) best = v;  // max(per_rank): first maximum
+    ps.add(v);
+  }
+  double t = gate + dispatch;
+  t = t + best;
+  t = t + dispatch;
+  *total = t;
+  if (ratio) {
+    const double sp = ps.result();
+    *ratio = sp > 0 ? best / (sp / (double)ep) : 1.0;
+  }
+  return FS_OK;
+}
 #else
 #define FFN_DENSE_US(c, n) dense_ffn_us(d, (c), (n))
 #endif
@@ -711,7 +902,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
       const int lend = min(L, l0 + kLayerChunk);
       double lane_ffn = 0.0, lane_ratio = 1.0;
       if (board) {
-        int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n);
+        int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n, sm->counts);
         if (st == FS_OK)
           st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, n, d->num_experts,
                                 d->top_k, d->d_model, d->expert_d_ff, d->ffn_matrices,
@@ -737,6 +928,12 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
           if (st != FS_OK) { fail(I, st, l); return 0.0; }
           I.routing_calls++;
           log_route(P, I, r, 0, step, l, n, sm);
+#if FS_LEARNED
+          if (d->gg_forest != -1)
+            st = learned_moe_layer_warp(P, I, sm, n, c.ep, c.moe_tp, c, &ffn,
+                                        moe_out ? &ratio : nullptr);
+          else
+#endif
           st = moe_layer_warp(I.lane, sm->counts, n, d->num_experts, d->top_k, d->d_model,
                               d->expert_d_ff, d->ffn_matrices, d->dtype_bytes, c.ep, c.moe_tp,
                               d->intra_latency_s, d->intra_bandwidth_bps, c, &ffn,
@@ -1377,7 +1574,7 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
       for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
         const int lend = min(L, l0 + kLayerChunk);
         if (board) {
-          int st = run_route_job(P, I, rd.prefix_mb, i + 1, step, l0, lend - l0, sz);
+          int st = run_route_job(P, I, rd.prefix_mb, i + 1, step, l0, lend - l0, sz, sm->counts);
           double lane_f = 0.0;
           if (st == FS_OK)
             st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, sz, d->num_experts,
@@ -1403,6 +1600,11 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
           I.routing_calls++;
           log_route(P, I, 0, i + 1, step, l, sz, sm);
           double f;
+#if FS_LEARNED
+          if (d->gg_forest != -1)
+            st = learned_moe_layer_warp(P, I, sm, sz, cf.ep, cf.moe_tp, cf, &f, nullptr);
+          else
+#endif
           st = moe_layer_warp(I.lane, sm->counts, sz, d->num_experts, d->top_k, d->d_model,
                               d->expert_d_ff, d->ffn_matrices, d->dtype_bytes, cf.ep, cf.moe_tp,
                               d->intra_latency_s, d->intra_bandwidth_bps, cf, &f, nullptr);
@@ -1542,8 +1744,6 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
 
   if (I.R > FS_MAX_REPLICAS || (d->has_moe && d->num_experts > FS_MAX_EXPERTS)) fail(I, FS_ERR_CAPACITY, 0);
 #if FS_LEARNED
-  // learned grouped GEMM on MoE layers needs numpy's np.log (load entropy): next
-  if (d->has_moe && d->gg_forest != -1) fail(I, FS_ERR_UNSUPPORTED, 101);
   {
     const int fsel[2] = {d->attn_forest, d->gg_forest};
     for (int k = 0; k < 2; k++) {
@@ -1648,7 +1848,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, FS_SIM_MIN_BLOCKS) sim_kern
     if (k >= P.n_inst) break;
     simulate_instance(P, P.order[k], lane, blockIdx.x * kWarpsPerCta + w, sm, slab);
   }
-  if (P.jobs) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w);
+  if (P.jobs) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w, sm->counts);
 }
 
 // Persistent grid: every CTA resident at once (the job board relies on warps

@@ -485,6 +485,64 @@ def learned_scenarios() -> dict[str, dict]:
     return s
 
 
+def learned_moe_fixtures() -> dict:
+    """Learned grouped-GEMM model on MoE layers (moe.py:95-106 -> model.py:323-327):
+    GroupedGemmFeatures(mode="local").vector() bits and predictions for per-rank
+    expert loads, plus whole MoE simulations costed with the model."""
+    from frontier_sim.costmodel.features import GroupedGemmFeatures
+    from frontier_sim.costmodel.model import load_model_file
+
+    gg_path = os.path.join("/tmp", "forest_gg_small.json")
+    with gzip.open(os.path.join(HERE, "forest_gg_small.json.gz"), "rt") as fh, \
+            open(gg_path, "w") as g:
+        g.write(fh.read())
+    model = load_model_file(gg_path)
+    rng = np.random.default_rng(77)
+    vecs = []
+    for i in range(400):
+        per = int(rng.choice([1, 2, 4, 7, 8, 16, 32, 33, 64, 128, 256]))
+        k = int(rng.integers(1, 9))
+        if i % 7 == 0:
+            counts = [0] * per
+            counts[int(rng.integers(0, per))] = int(rng.integers(1, 5000))
+        else:
+            lam = float(rng.choice([0.3, 2.0, 40.0, 900.0]))
+            counts = [int(x) for x in rng.poisson(lam, size=per)]
+        if sum(counts) == 0:
+            counts[0] = 1
+        dm = int(rng.choice([1024, 4096, 7168])); dff = int(rng.choice([256, 2048, 14336]))
+        f = GroupedGemmFeatures(total_tokens=sum(counts), expert_token_counts=tuple(counts),
+                                d_model=dm, d_ff=dff, top_k=k, mode="local")
+        v = f.vector()
+        vecs.append([counts, dm, dff, k, [int(x) for x in v.view(np.uint64)],
+                     model.predict_us(v)])
+    sims = {}
+    gg = {"mode": "learned", "grouped_gemm_model": "forest_gg_small.json"}
+    both = {"mode": "learned", "attention_model": "forest_small.json",
+            "grouped_gemm_model": "forest_gg_small.json"}
+    d = copy.deepcopy(W.c5_sweep_configs(24)[48 + 5])  # Mixtral ep=2
+    d["seed"] = 31
+    d["cost_model"] = dict(gg)
+    sims["learned_gg_mixtral_ep2"] = d
+    d = copy.deepcopy(scenarios()["af_tiny_moe_m3_dp2"])
+    d["seed"] = 32
+    d["cost_model"] = dict(both)
+    sims["learned_both_af_tiny_moe"] = d
+    d = W.c4_colocated_ep(6, seed=33)
+    d["cost_model"] = dict(gg)
+    sims["learned_gg_dsv3_ep8"] = d
+    d = copy.deepcopy(scenarios()["co_tiny_moe_gated_ep4"])
+    d["seed"] = 34
+    d["cost_model"] = dict(gg)
+    sims["learned_gg_tiny_moe_gated"] = d
+    out = {"gg_vectors": vecs,
+           "scenarios": {n: record(doc, with_batches=True, with_routes=True, base_dir="/tmp")
+                         for n, doc in sims.items()}}
+    for name, r in out["scenarios"].items():
+        print(name, r.get("iterations"), r.get("error"), f"{r['wall_s']:.2f}s")
+    return out
+
+
 def dirichlet_fixtures() -> dict:
     """dirichlet_skew routing (routing.py:99-106): route_tokens counts from the
     reference, the raw stream (popularity + first key row) from the reference's
@@ -562,6 +620,8 @@ def main() -> None:
             print(name, sc[name].get("iterations"), sc[name].get("error"),
                   f"{sc[name]['wall_s']:.2f}s")
         write("scenarios", sc)
+    if only is None or "learned_moe" in only:
+        write("learned_moe", learned_moe_fixtures())
     if only is None or "dirichlet" in only:
         write("dirichlet", dirichlet_fixtures())
     if only is None or "forest" in only:

@@ -139,3 +139,40 @@ def test_gpu_simulate_learned_failures(engine, model_dir, golden_learned):
             assert isinstance(o, Failure) and type(o.exception).__name__ == "SchemaMismatch", n
         else:
             assert not isinstance(o, Failure), (n, o)
+
+
+# -- learned grouped-GEMM model on MoE layers (moe.py:95-106, model.py:323-326) --------------
+
+@pytest.fixture(scope="module")
+def golden_learned_moe():
+    from conftest import load_golden
+    return load_golden("learned_moe")["data"]
+
+
+def test_oracle_gg_local_feature_vectors(model_dir, golden_learned_moe):
+    """GroupedGemmFeatures(..., "local").vector() bits and predictions (400 rank loads)."""
+    from oracle import oracle
+    fs = costmodel.ForestSet()
+    fs.add(costmodel.load_model_file(os.path.join(model_dir, "forest_gg_small.json")))
+    for counts, dm, dff, k, bits, pred in golden_learned_moe["gg_vectors"]:
+        x, v = oracle.gg_features(counts, dm, dff, k, fs, 0)
+        assert x.view(np.uint64).tolist() == bits, counts
+        assert v == pred, counts
+
+
+def test_oracle_learned_moe_scenarios(model_dir, golden_learned_moe):
+    sc = golden_learned_moe["scenarios"]
+    names = list(sc)
+    res = run_backend("oracle", [sc[n]["config"] for n in names], routes=True, threads=4,
+                      base_dir=model_dir)
+    bad = {n: compare_to_golden(r, sc[n]) for n, r in zip(names, res)}
+    assert {n: b for n, b in bad.items() if b} == {}
+
+
+@pytest.mark.gpu
+def test_gpu_learned_moe_scenarios(engine, model_dir, golden_learned_moe):
+    sc = golden_learned_moe["scenarios"]
+    names = list(sc)
+    res = run_backend(engine, [sc[n]["config"] for n in names], routes=True, base_dir=model_dir)
+    bad = {n: compare_to_golden(r, sc[n]) for n, r in zip(names, res)}
+    assert {n: b for n, b in bad.items() if b} == {}
