@@ -166,18 +166,23 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+def ncu_summary(kernel: str) -> dict:
+    """`kernel`'s entry in the committed ncu --set full summary (profiles/)."""
     path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
         for name, v in d.items():  # kernel variants carry a suffix (e.g. _tpb)
             if name == kernel or name.startswith(kernel + "_"):
-                return v.get("dram_bytes_per_launch")
-        return None
+                return v
     except Exception:
-        return None
+        pass
+    return {}
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    return ncu_summary(kernel).get("dram_bytes_per_launch")
 
 
 def algorithmic_bytes(low, rows) -> int:
@@ -377,6 +382,21 @@ def main():
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     traffic = ncu_traffic("sim_kernel")
 
+    # the DES step kernel is instruction-issue bound, not HBM bound: its
+    # instruction roofline from the committed ncu capture (warp instructions per
+    # launch, same workload) over this run's step time vs 148 SMs x 4 issue/clk
+    issue = None
+    summ = ncu_summary("sim_kernel")
+    if summ.get("warp_instructions"):
+        sm_mhz = (clocks.summary() or {}).get("sm_max_mhz") or 1965.0
+        peak_ips = 148 * 4 * sm_mhz * 1e6
+        ips = summ["warp_instructions"] / (avg_ms / 1e3)
+        issue = {"bound": "issue", "unit": "warp-instructions/s", "achieved": ips,
+                 "peak": peak_ips, "frac": ips / peak_ips,
+                 "warp_instructions_per_launch": summ["warp_instructions"],
+                 "ncu_issue_active_pct": summ.get("issue_active_pct"),
+                 "source": summ.get("source")}
+
     c2 = None
     if not args.no_c2:
         c2 = bench_attention_cost(eng, local, args.steps, args.warmup)
@@ -407,6 +427,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "sim_kernel (+metrics_kernel)",
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
+            "issue": issue,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -58,6 +59,9 @@ struct fs_engine {
   DevBuf f_descs, f_roots, f_right, f_value, f_leaf;  // f_value: packed NodeP array
   fs::ForestView fv{};
   bool learned = false;  // staged batch uses the learned simulation variant
+  // routing job geometry (environment knobs read at fs_create)
+  int sim_ctas = 0;          // FS_SIM_CTAS_PER_SM (0 = as many as fit)
+  int chunk_blocks = 96;     // FS_CHUNK_BLOCKS: Philox blocks per lane per job chunk
   int32_t n_inst = 0, n_reps = 0, n_prefixes = 0;
   int64_t n_req = 0;
   int staged = 0;
@@ -108,6 +112,12 @@ int fs_create(int device, fs_engine** out) {
   fs_engine* e = new fs_engine();
   e->device = device;
   cudaDeviceGetAttribute(&e->n_sms, cudaDevAttrMultiProcessorCount, device);
+  auto env_int = [](const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+  };
+  e->sim_ctas = env_int("FS_SIM_CTAS_PER_SM", 0);
+  e->chunk_blocks = env_int("FS_CHUNK_BLOCKS", 96);
   if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete e;
     return 5;
@@ -120,6 +130,7 @@ void fs_destroy(fs_engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamDestroy(e->stream);
+
   delete e;
 }
 
@@ -257,7 +268,8 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
     // dirichlet_skew routing is compiled into the extended (learned) kernel variant only
     if (descs[i].has_moe && descs[i].routing_policy == FS_ROUTE_DIRICHLET) e->learned = true;
   }
-  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned);
+  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned, e->sim_ctas);
+  P.chunk_blocks = e->chunk_blocks;
   int max_e = 0;
   for (int i = 0; i < n_instances; i++)
     if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);

@@ -93,6 +93,7 @@ struct EngineParams {
   int32_t* inst_done;            // instances finished (helpers stop at n_inst)
   int32_t* open_jobs;            // published jobs with unclaimed chunks
   double* dir_scratch;           // [n_slots][kDirScratch]: dirichlet_skew popularity + key ring
+  int32_t chunk_blocks;          // Philox blocks per lane per chunk (FS_CHUNK_BLOCKS)
   ForestView fv;                 // learned operator models (fs_set_forests)
 };
 
@@ -100,14 +101,15 @@ struct EngineParams {
 void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void* stream);
 // simulation kernel variants (fs_sim.cuh compiled twice)
 namespace analytic {
-int slots(int n_sms, int n_inst);
+int slots(int n_sms, int n_inst, int ctas_per_sm);
 int launch(const EngineParams& p, void* stream);
 }  // namespace analytic
 namespace learned {
-int slots(int n_sms, int n_inst);
+int slots(int n_sms, int n_inst, int ctas_per_sm);
 int launch(const EngineParams& p, void* stream);
 }  // namespace learned
-int simulation_slots(int n_sms, int n_inst, bool learned);
+// ctas_per_sm <= 0: as many simulation CTAs per SM as fit
+int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm);
 int launch_simulation(const EngineParams& p, bool learned, void* stream);
 int launch_metrics(const EngineParams& p, void* stream);
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,

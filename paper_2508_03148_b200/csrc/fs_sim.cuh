@@ -49,6 +49,12 @@
 #ifndef FS_DIR_IN_ANALYTIC
 #define FS_DIR_IN_ANALYTIC 0
 #endif
+#ifndef FS_ROW8_FAST  // straight-line routing pass for whole 8-draw row segments
+#define FS_ROW8_FAST 0
+#endif
+#ifndef FS_COLD_NOINLINE  // rare routing paths out of line (compact hot code)
+#define FS_COLD_NOINLINE 0
+#endif
 
 namespace fs {
 namespace FS_SIM_NS {
@@ -236,6 +242,15 @@ __device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int pref
   __syncwarp();
 }
 
+#if FS_COLD_NOINLINE
+// the owning-warp uniform router: only the RNG-free shortcuts and jobs the board
+// does not take reach it in a sweep, so it stays out of line
+__device__ __noinline__ int route_uniform_cold(int lane, int64_t T, int E, int k, uint64_t k0,
+                                               uint64_t k1, int* counts) {
+  return route_uniform_warp(lane, T, E, k, k0, k1, counts);
+}
+#endif
+
 // ---- one router call (routing.py:65-113) ------------------------------------------------
 __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
                            uint64_t k0, uint64_t k1, WarpSmem* sm) {
@@ -264,7 +279,11 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
   if (T == 0 || k == E || policy == FS_ROUTE_UNIFORM) {
     if (T > 0 && k < E && k > FS_MAX_TOPK) return FS_ERR_CAPACITY;
     __syncwarp();
+#if FS_COLD_NOINLINE
+    return route_uniform_cold(I.lane, T, E, k, k0, k1, sm->counts);
+#else
     return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
+#endif
   }
 #if FS_LEARNED || FS_DIR_IN_ANALYTIC
   // dirichlet_skew instances run in the extended (learned) variant of this kernel:
@@ -311,8 +330,8 @@ __device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t
 constexpr unsigned kChunkBits = 20;
 constexpr unsigned long long kChunkMask = (1ull << kChunkBits) - 1;
 constexpr int kMaxChunks = 1 << 18;
-#ifndef FS_CHUNK_BLOCKS  // Philox blocks per lane per claimed chunk
-#define FS_CHUNK_BLOCKS 48
+#ifndef FS_CHUNK_BLOCKS  // Philox blocks per lane per claimed chunk (96: 267 ms, 48: 276, 16: 350)
+#define FS_CHUNK_BLOCKS 96
 #endif
 constexpr int kChunkBlocks = FS_CHUNK_BLOCKS;
 
@@ -401,6 +420,41 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
       }
     }
   };
+#if FS_ROW8_FAST
+  if (((n0 | n1) & 7) == 0) {
+    // the row segment is whole 8-draw groups (E a multiple of 8, one segment
+    // per row): block pairs, no range predicates, two blocks in flight
+    for (uint64_t b = n0 >> 2; b < (n1 >> 2); b += 2) {
+      U4 A, B;
+#if FS_ROW8_FAST >= 2
+      philox4x64_10_x2(b + 1, b + 2, k0, k1, A, B);
+#else
+      A = philox4x64_10(b + 1, k0, k1);
+      B = philox4x64_10(b + 2, k0, k1);
+#endif
+      const uint32_t eb0 = (uint32_t)(4 * b - rb);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const uint64_t w = j < 4 ? A.v[j] : B.v[j - 4];
+        uint32_t x = ((uint32_t)(w >> 32) & ~emask) | (eb0 + (uint32_t)j);
+        if (KCAP <= 4 || x < thr) {
+#pragma unroll
+          for (int q = 0; q < KCAP; q++) {
+            const uint32_t lo = min(top[q], x);
+            x = max(top[q], x);
+            top[q] = lo;
+          }
+          if (KCAP > 4) {
+#pragma unroll
+            for (int q = 0; q < KCAP; q++)
+              if (q == kc - 1) thr = top[q];
+          }
+        }
+      }
+    }
+    return;
+  }
+#endif
 #if FS_PHILOX_ILP >= 2
   // two blocks per step (a trailing odd block is generated and ignored)
   const uint64_t blast = (n1 - 1) >> 2;
@@ -414,6 +468,37 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
   for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) consume(philox4x64_10(b + 1, k0, k1), b);
 #endif
 }
+
+#if FS_COLD_NOINLINE
+// Exact 64-bit redo of one pass (the 32-bit surrogate keys tied at the k-th /
+// (k+1)-th boundary): rare, so out of line to keep the hot loop's code compact.
+// Fills ids[] and returns 1 on a true boundary tie.
+template <int KCAP>
+__device__ __noinline__ int exact_redo(int (&ids)[KCAP], bool active, bool leader, int e0, int e1,
+                                       uint64_t rb, int nseg, int k, uint64_t k0, uint64_t k1) {
+  const int kc = k + 1;
+  uint64_t t64[KCAP];
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
+  uint64_t thr = ~0ull;
+  if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
+  for (int s = 1; s < nseg; s <<= 1) {
+    uint64_t other[KCAP];
+#pragma unroll
+    for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
+#pragma unroll
+    for (int j = 0; j < KCAP; j++)
+      if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
+  }
+  int tie = 0;
+#pragma unroll
+  for (int j = 0; j < KCAP; j++) {
+    ids[j] = (int)(t64[j] & 0x7FF);
+    if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
+  }
+  return tie;
+}
+#endif
 
 template <int KCAP>
 __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
@@ -483,6 +568,9 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
 #pragma unroll
     for (int j = 0; j < KCAP; j++) ids[j] = (int)(top[j] & emask);
     if (__any_sync(FS_FULL, unsure)) {
+#if FS_COLD_NOINLINE
+      tie |= exact_redo<KCAP>(ids, active, leader, e0, e1, rb, nseg, k, k0, k1);
+#else
       // exact 64-bit redo of this pass
       uint64_t t64[KCAP];
 #pragma unroll
@@ -502,6 +590,7 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
         ids[j] = (int)(t64[j] & 0x7FF);
         if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
       }
+#endif
     }
     if (local) {
       if (leader) {
@@ -606,7 +695,7 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
   const int rpp = 32 / nseg;
   const int64_t passes = (rows + rpp - 1) / rpp;
   const int blocks_per_pass = ((E + nseg - 1) / nseg + 3) / 4 + 1;
-  int ppc = kChunkBlocks / blocks_per_pass;
+  int ppc = (P.chunk_blocks > 0 ? P.chunk_blocks : kChunkBlocks) / blocks_per_pass;
   if (ppc < 1) ppc = 1;
   int64_t n_chunks = (passes + ppc - 1) / ppc;
   if (n_chunks > kMaxChunks) {
@@ -1863,10 +1952,11 @@ static size_t sim_dyn_smem() {
   return bytes;
 }
 
-int slots(int n_sms, int n_inst) {
+int slots(int n_sms, int n_inst, int ctas_per_sm) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel, 32 * kWarpsPerCta,
                                                 sim_dyn_smem());
+  if (ctas_per_sm > 0 && ctas_per_sm < per_sm) per_sm = ctas_per_sm;
   if (per_sm < 1) per_sm = 1;
   const int need = (n_inst + kWarpsPerCta - 1) / kWarpsPerCta;
   int grid = n_sms * per_sm;

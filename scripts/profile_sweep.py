@@ -13,7 +13,12 @@ from paper_2508_03148_b200.engine import Engine  # noqa: E402
 
 def main():
     seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-    low = lower_docs(workload_docs(0, seeds, 64))
+    docs = workload_docs(0, seeds, 64)
+    fams = os.environ.get("FS_FAMILIES")  # e.g. "AB": profile a subset of the C5 families
+    if fams:
+        fam_of = ["A"] * 16 + ["B"] * 32 + ["C"] * 16
+        docs = [d for i, d in enumerate(docs) if fam_of[i // seeds] in fams]
+    low = lower_docs(docs)
     eng = Engine(0)
     eng.stage(low)
     for _ in range(2):
@@ -29,6 +34,8 @@ def main():
     wall = time.perf_counter() - t0
     its = res.rows["iterations"]
     fam = np.repeat(np.array(["A"] * 16 + ["B"] * 32 + ["C"] * 16), seeds)
+    if fams:
+        fam = np.array([f for f in fam if f in fams])
     print(f"sweep wall {wall*1e3:.1f} ms, iterations {its.sum()}, it/s {its.sum()/wall:.3e}")
     clk = 1.965e9
     for f in "ABC":

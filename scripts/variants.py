@@ -3,6 +3,8 @@
   python scripts/variants.py build NAME "-DFLAG=1 ..." [NAME "FLAGS" ...]
       compiles fs_engine.cu with the flags into paper_2508_03148_b200/lib/variants/NAME.so
       (linked with the standard objects of the other translation units)
+  python scripts/variants.py timeenv SEEDS "FS_X=1,FS_Y=2" ...
+      GPU: the default library under runtime knobs (environment), one process each
   python scripts/variants.py time [seeds] [NAME ...]
       GPU: for the default library and each variant, one process that stages the C5
       sweep and times 3 launches with CUDA events (prints one JSON line each)
@@ -76,6 +78,17 @@ def time_all(seeds: int, names):
         subprocess.run([sys.executable, __file__, "_one", str(seeds)], env=env, timeout=600)
 
 
+def time_envs(seeds: int, envs):
+    """Runtime knobs (fs_capi.cu reads FS_* at fs_create): one process per setting."""
+    for spec in [""] + list(envs):
+        env = dict(os.environ)
+        for kv in filter(None, spec.split(",")):
+            k, v = kv.split("=")
+            env[k] = v
+        print("env:", spec or "(defaults)", flush=True)
+        subprocess.run([sys.executable, __file__, "_one", str(seeds)], env=env, timeout=600)
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "build":
@@ -84,5 +97,7 @@ if __name__ == "__main__":
     elif cmd == "time":
         seeds = int(sys.argv[2]) if len(sys.argv) > 2 else 64
         time_all(seeds, sys.argv[3:])
+    elif cmd == "timeenv":
+        time_envs(int(sys.argv[2]), sys.argv[3:])
     elif cmd == "_one":
         time_one(int(sys.argv[2]))
