@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 attention-cost kernel leg")
-    ap.add_argument("--cpu-sample-seeds", type=int, default=2)
+    ap.add_argument("--cpu-sample-seeds", type=int, default=8)
     return ap.parse_args()
 
 
@@ -310,6 +310,7 @@ def main():
         bad = int((res.rows["status"] != 0).sum())
         raise SystemExit(f"{bad} instances failed: statuses {np.unique(res.rows['status'])}")
     iters_per_step = int(res.rows["iterations"].sum())
+    draws_per_step = int(res.rows["routing_draws"].sum())
     launches_per_step = eng.last_launch_count
 
     # timed region: device-resident inputs
@@ -405,10 +406,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_count()
         c_its, c_dt, n_inst = run_oracle_sample(args.requests, args.cpu_sample_seeds, threads)
+        s_its, s_dt, s_inst = run_oracle_sample(args.requests, 1, 1)  # one core, serial
         cpu = {"value": c_its / c_dt, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"C5 configs x {args.cpu_sample_seeds} seeds = {n_inst} instances "
                          f"({c_its} iterations) in {c_dt:.2f}s on {threads} threads "
-                         f"({cpu_model()}); oracle/fs_oracle.c"}
+                         f"({cpu_model()}); oracle/fs_oracle.c",
+               "serial_1core": {"value": s_its / s_dt, "unit": UNIT,
+                                "sample": f"C5 configs x 1 seed = {s_inst} instances "
+                                          f"({s_its} iterations) in {s_dt:.2f}s"}}
 
     if rank == 0:
         line = {
@@ -428,6 +433,10 @@ def main():
                          "kernel": "sim_kernel (+metrics_kernel)",
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
             "issue": issue,
+            "routing": {"draws_per_step": draws_per_step * world,
+                        "draws_per_s": draws_per_step * world / (max_ms / args.steps / 1e3),
+                        "note": "uniform-router Philox4x64-10 keys (T x E per call) drawn "
+                                "inside sim_kernel"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps,

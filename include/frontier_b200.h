@@ -209,6 +209,7 @@ typedef struct {
   double af_busy_fraction[4];
   int64_t moe_layer_samples;  /* number of moe_imbalance entries (base.py:247-252) */
   int64_t routing_calls;
+  int64_t routing_draws;      /* router keys drawn: T x E per call with random keys */
 } fs_metric_row;
 
 typedef struct {

@@ -430,6 +430,7 @@ typedef struct Sim {
   /* routing log */
   fs_log* log; int inst;
   int64_t routing_calls;
+  int64_t routing_draws;
   int32_t log_moff, log_eoff;
   /* errors */
   jmp_buf jb;
@@ -735,6 +736,7 @@ static int64_t* route(Sim* s, int64_t T, uint32_t seed, int policy_uniform_force
   } else {
     int st = route_core(T, E, k, policy, d->routing_alpha, (uint64_t)seed, counts);
     if (st) { free(counts); fail(s, st, 0); }
+    s->routing_draws += T * E;
   }
   s->routing_calls++;
   fs_log* lg = s->log;
@@ -1579,6 +1581,7 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
   row->iterations = row->prefill_batches + row->decode_batches + row->af_steps;
   row->n_requests = N;
   row->routing_calls = s->routing_calls;
+  row->routing_draws = s->routing_draws;
   if (s->status == FS_OK && N > 0) {
     /* compute_metrics (metrics.py:81-178) */
     double* tt = (double*)malloc(sizeof(double) * (size_t)N * 3);

@@ -64,7 +64,7 @@ METRIC_ROW = np.dtype([
     ("ttft", "<f8", (4,)), ("tpot", "<f8", (4,)), ("e2e", "<f8", (4,)),
     ("bubble_fraction", "<f8"), ("avg_input_tokens", "<f8"), ("avg_output_tokens", "<f8"),
     ("af_busy_ns", "<i8", (4,)), ("af_busy_fraction", "<f8", (4,)),
-    ("moe_layer_samples", "<i8"), ("routing_calls", "<i8"),
+    ("moe_layer_samples", "<i8"), ("routing_calls", "<i8"), ("routing_draws", "<i8"),
 ], align=True)
 
 REPLICA_OUT = np.dtype([("busy_ns", "<i8"), ("busy_fraction", "<f8"),

@@ -98,7 +98,7 @@ struct Inst {
   int64_t af_busy[4];
   double bubble_weighted;
   int64_t bubble_total;
-  int64_t prefill_batches, decode_batches, af_steps, moe_samples, routing_calls;
+  int64_t prefill_batches, decode_batches, af_steps, moe_samples, routing_calls, routing_draws;
   int32_t log_batches, log_moff, log_eoff, log_routes;
 };
 
@@ -250,6 +250,12 @@ __device__ __noinline__ int route_uniform_cold(int lane, int64_t T, int E, int k
   return route_uniform_warp(lane, T, E, k, k0, k1, counts);
 }
 #endif
+
+// keys a router call draws (T x E; none for the trace policy and the RNG-free shortcuts)
+__device__ __forceinline__ int64_t draws_of(const fs_instance_desc* d, int policy, int64_t T) {
+  return (policy != FS_ROUTE_TRACE && T > 0 && d->top_k < d->num_experts)
+             ? T * (int64_t)d->num_experts : 0;
+}
 
 // ---- one router call (routing.py:65-113) ------------------------------------------------
 __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int64_t T,
@@ -1008,6 +1014,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
           ffn = __shfl_sync(FS_FULL, lane_ffn, l - l0);
           ratio = __shfl_sync(FS_FULL, lane_ratio, l - l0);
           I.routing_calls++;
+          I.routing_draws += draws_of(d, FS_ROUTE_UNIFORM, n);
           if (log_routes) {
             load_job_layer(P, I, l - l0, sm);
             log_route(P, I, r, 0, step, l, n, sm);
@@ -1016,6 +1023,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
           int st = route_layer(P, I, d->routing_policy, n, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
           if (st != FS_OK) { fail(I, st, l); return 0.0; }
           I.routing_calls++;
+          I.routing_draws += draws_of(d, d->routing_policy, n);
           log_route(P, I, r, 0, step, l, n, sm);
 #if FS_LEARNED
           if (d->gg_forest != -1)
@@ -1673,6 +1681,7 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
           if (st != FS_OK) { fail(I, st, l0); return; }
           if (I.lane < lend - l0) ffn[(int64_t)i * L + l0 + I.lane] = py_round(lane_f * 1000.0);
           I.routing_calls += lend - l0;
+          I.routing_draws += (lend - l0) * draws_of(d, FS_ROUTE_UNIFORM, sz);
           if (P.log_enabled && P.log.routes) {
             for (int l = l0; l < lend; l++) {
               load_job_layer(P, I, l - l0, sm);
@@ -1687,6 +1696,7 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
           int st = route_layer(P, I, FS_ROUTE_UNIFORM, sz, sm->keys[l - l0][0], sm->keys[l - l0][1], sm);
           if (st != FS_OK) { fail(I, st, l); return; }
           I.routing_calls++;
+          I.routing_draws += draws_of(d, FS_ROUTE_UNIFORM, sz);
           log_route(P, I, 0, i + 1, step, l, sz, sm);
           double f;
 #if FS_LEARNED
@@ -1829,6 +1839,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
   I.bubble_weighted = 0.0;
   I.bubble_total = 0;
   I.prefill_batches = I.decode_batches = I.af_steps = I.moe_samples = I.routing_calls = 0;
+  I.routing_draws = 0;
   I.log_batches = I.log_moff = I.log_eoff = I.log_routes = 0;
 
   if (I.R > FS_MAX_REPLICAS || (d->has_moe && d->num_experts > FS_MAX_EXPERTS)) fail(I, FS_ERR_CAPACITY, 0);
@@ -1897,6 +1908,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
     row.af_steps = I.af_steps;
     row.iterations = I.prefill_batches + I.decode_batches + I.af_steps;
     row.routing_calls = I.routing_calls;
+    row.routing_draws = I.routing_draws;
     row.moe_layer_samples = d->has_moe ? (I.prefill_batches + I.decode_batches) * (int64_t)d->num_layers : 0;
     row.n_requests = I.N;
     for (int k = 0; k < 4; k++) row.af_busy_ns[k] = I.af_busy[k];

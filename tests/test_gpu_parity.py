@@ -21,7 +21,8 @@ pytestmark = pytest.mark.gpu
 ROW_FIELDS = ("status", "iterations", "events", "total_tokens", "makespan_ns", "prefill_batches",
               "decode_batches", "af_steps", "n_tpot", "makespan_s",
               "throughput_tokens_per_s_per_gpu", "ttft", "tpot", "e2e", "avg_input_tokens",
-              "avg_output_tokens", "af_busy_ns", "af_busy_fraction", "routing_calls")
+              "avg_output_tokens", "af_busy_ns", "af_busy_fraction", "routing_calls",
+              "routing_draws")
 
 
 def assert_same_raw(dev, ref):
