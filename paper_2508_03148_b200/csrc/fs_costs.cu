@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "fs_device.cuh"
 #include "fs_engine.h"
@@ -183,6 +184,37 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_u(
   }
 }
 
+// A batch's roofline from its integer reductions (analytic.py:32-53): decode
+// flops from sum(kv); prefill flops as the exact integer sum while every partial
+// sum stays below 2^53 (equal to Python's sequential fp64 sum), else the
+// sequential fp64 loop in member order. NaN + status for invalid batches.
+__device__ __forceinline__ void c2_finish(int64_t b, bool d, int64_t sq, int64_t skv, int64_t seq,
+                                          int64_t sne, int64_t mlc, int bad, int64_t o0,
+                                          int64_t o1, const int32_t* __restrict__ q,
+                                          const int32_t* __restrict__ kv,
+                                          const fs_attn_params& prm, const fs_cost_ctx& h,
+                                          double* __restrict__ out, int32_t* __restrict__ status) {
+  const int64_t hd = (int64_t)prm.num_query_heads * prm.head_dim;
+  const int st = o1 <= o0 ? FS_ERR_EMPTY_BATCH : (bad ? FS_ERR_VALUE : FS_OK);
+  double flops;
+  if (d) {
+    sq = o1 - o0;  // every q is 1 unless `bad`
+    flops = attention_decode_flops(skv, hd);
+  } else {
+    const double est = 4.0 * (double)hd * ((double)sne + 0.5 * (double)seq);
+    if (4.0 * (double)mlc * (double)hd < kTwo53 * 0.5 && est < kTwo53 * 0.5) {
+      flops = i2d(4 * hd * sne + 2 * hd * seq);  // exact integer sum == sequential fp64 sum
+    } else {
+      flops = 0.0;  // sequential, member order (analytic.py:37-43)
+      for (int64_t j = o0; j < o1; j++) flops = flops + attention_prefill_term(q[j], kv[j], hd);
+    }
+  }
+  const double us = attention_us_from(flops, sq, skv, prm.num_query_heads, prm.num_kv_heads,
+                                      prm.head_dim, h, prm.dtype_bytes);
+  out[b] = st == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
+  if (status) status[b] = st;
+}
+
 // Thread per batch: each thread streams its own batch's (q, kv) lengths with
 // 128-bit loads (scalar head/tail to the 16-byte boundary) and accumulates in
 // registers -- no cross-lane reduction at all, so a 72-request batch costs a
@@ -227,24 +259,161 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_tpb(
       x.n = 1;
       acc4(sq, skv, seq, sne, mlc, bad, x, d);
     }
-    int st = o1 <= o0 ? FS_ERR_EMPTY_BATCH : (bad ? FS_ERR_VALUE : FS_OK);
-    double flops;
-    if (d) {
-      sq = o1 - o0;  // every q is 1 unless `bad`
-      flops = attention_decode_flops(skv, hd);
-    } else {
-      const double est = 4.0 * (double)hd * ((double)sne + 0.5 * (double)seq);
-      if (4.0 * (double)mlc * (double)hd < kTwo53 * 0.5 && est < kTwo53 * 0.5) {
-        flops = i2d(4 * hd * sne + 2 * hd * seq);  // exact integer sum == sequential fp64 sum
+    c2_finish(b, d, sq, skv, seq, sne, mlc, bad, o0, o1, q, kv, prm, h, out, status);
+  }
+}
+
+// ---- TMA-staged variant ----------------------------------------------------------------------
+// The CSR length arrays are one contiguous stream per tile, so the whole tile
+// (kC2TileBatches batches: their q and kv ranges, widened to 16-byte bounds) is
+// moved into shared memory by two cp.async.bulk copies that complete on an
+// mbarrier -- no per-thread address streams, no L1 thrash, DRAM reads at the
+// algorithmic bytes. A kC2Stages-deep ring keeps that many tiles in flight per
+// CTA. Four threads reduce one batch with 128-bit shared-memory loads (thread j
+// of a group takes the int4 groups j, j+4, ...; scalar when the batch does not
+// start on a 16-byte boundary), partial sums meet by shuffle, and the group
+// leader runs the fp64 tail. A tile that does not fit a stage (long batches) or
+// whose widened range would read past the arrays runs from global memory.
+constexpr int kC2TileBatches = 32;   // 4 warps x 8 batches
+constexpr int kC2Threads = 128;      // 4 threads per batch
+constexpr int kC2Stages = 4;
+constexpr int kC2StageElems = 2560;  // per array: 32 x 72 members + alignment slack
+
+struct C2Smem {
+  int32_t q[kC2Stages][kC2StageElems];
+  int32_t kv[kC2Stages][kC2StageElems];
+  unsigned long long full[kC2Stages];
+  int64_t base[kC2Stages];   // element index of q[stage][0], or -1: read from global
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// producer: thread 0 stages tile `t` into `st` (or marks it for the global path)
+__device__ __forceinline__ void c2_issue(C2Smem& S, int st, int64_t t, int64_t nb,
+                                         const int32_t* q, const int32_t* kv, const int64_t* off,
+                                         bool aligned) {
+  const int64_t b0 = t * kC2TileBatches;
+  const int64_t b1 = min(nb, b0 + kC2TileBatches);
+  const int64_t e0 = __ldg(off + b0), e1 = __ldg(off + b1), eN = __ldg(off + nb);
+  const int64_t a0 = e0 & ~(int64_t)3, a1 = (e1 + 3) & ~(int64_t)3;
+  const uint32_t bar = smem_u32(&S.full[st]);
+  if (!aligned || a1 - a0 > kC2StageElems || a1 > eN || a1 <= a0) {
+    S.base[st] = -1;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    return;
+  }
+  S.base[st] = a0;
+  const uint32_t bytes = (uint32_t)((a1 - a0) * 4);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(&S.q[st][0])), "l"(q + a0), "r"(bytes), "r"(bar)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(&S.kv[st][0])), "l"(kv + a0), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void c2_wait(C2Smem& S, int st, uint32_t parity) {
+  const uint32_t bar = smem_u32(&S.full[st]);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "C2_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra C2_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kC2Threads) attention_cost_kernel_tma(
+    const int32_t* __restrict__ q, const int32_t* __restrict__ kv,
+    const int64_t* __restrict__ off, const uint8_t* __restrict__ dec, int64_t nb,
+    fs_attn_params prm, double* __restrict__ out, int32_t* __restrict__ status) {
+  extern __shared__ __align__(128) unsigned char c2_raw[];
+  C2Smem& S = *reinterpret_cast<C2Smem*>(c2_raw);
+  fs_cost_ctx h;
+  h.peak_flops = prm.peak_flops; h.mem_bw = prm.mem_bw; h.kernel_overhead_us = prm.kernel_overhead_us;
+  h.tp = h.ep = h.moe_tp = h.pp = 1;
+  const int tid = threadIdx.x, grp = tid >> 2, j = tid & 3;
+  const int64_t n_tiles = (nb + kC2TileBatches - 1) / kC2TileBatches;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv)) & 15) == 0;
+  if (tid == 0) {
+    for (int s = 0; s < kC2Stages; s++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.full[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kC2Stages; s++) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < n_tiles) c2_issue(S, s, t, nb, q, kv, off, aligned);
+    }
+  }
+  __syncthreads();
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, it++) {
+    const int st = it % kC2Stages;
+    c2_wait(S, st, (uint32_t)((it / kC2Stages) & 1));
+    const int64_t base = S.base[st];
+    const int64_t b = t * kC2TileBatches + grp;
+    int64_t sq = 0, skv = 0, sall = 0, seq = 0, o0 = 0, o1 = 0;
+    int bad = 0, ml = 0, mc = 0;
+    bool d = false;
+    auto member = [&](int l, int c) {
+      skv += c;
+      bad |= (l < 1) | (c < 1) | (d ? (l != 1) : (c < l));
+      if (!d) {
+        sq += l;
+        const int64_t lc = (int64_t)l * c;
+        sall += lc;
+        seq += (c == l) ? lc : 0;
+        ml = max(ml, l);
+        mc = max(mc, c);
+      }
+    };
+    if (b < nb) {
+      o0 = __ldg(off + b);
+      o1 = __ldg(off + b + 1);
+      d = __ldg(dec + b) != 0;
+      if (base >= 0 && ((o0 - base) & 3) == 0) {
+        const int4* qv = reinterpret_cast<const int4*>(&S.q[st][o0 - base]);
+        const int4* kvv = reinterpret_cast<const int4*>(&S.kv[st][o0 - base]);
+        const int n4 = (int)((o1 - o0) >> 2);
+        for (int i = j; i < n4; i += 4) {
+          const int4 a = qv[i], c = kvv[i];
+          member(a.x, c.x); member(a.y, c.y); member(a.z, c.z); member(a.w, c.w);
+        }
+        const int64_t tail = o0 + 4 * (int64_t)n4 + j;
+        if (tail < o1) member(S.q[st][tail - base], S.kv[st][tail - base]);
       } else {
-        flops = 0.0;  // sequential, member order (analytic.py:37-43)
-        for (int64_t j = o0; j < o1; j++) flops = flops + attention_prefill_term(q[j], kv[j], hd);
+        const int32_t* sqp = base >= 0 ? &S.q[st][0] - base : q;
+        const int32_t* skp = base >= 0 ? &S.kv[st][0] - base : kv;
+        for (int64_t i = o0 + j; i < o1; i += 4) member(sqp[i], skp[i]);
       }
     }
-    const double us = attention_us_from(flops, sq, skv, prm.num_query_heads, prm.num_kv_heads,
-                                        prm.head_dim, h, prm.dtype_bytes);
-    out[b] = st == FS_OK ? us : __longlong_as_double(0x7ff8000000000000LL);
-    if (status) status[b] = st;
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      sq += __shfl_xor_sync(FS_FULL, sq, o);
+      skv += __shfl_xor_sync(FS_FULL, skv, o);
+      sall += __shfl_xor_sync(FS_FULL, sall, o);
+      seq += __shfl_xor_sync(FS_FULL, seq, o);
+      ml = max(ml, __shfl_xor_sync(FS_FULL, ml, o));
+      mc = max(mc, __shfl_xor_sync(FS_FULL, mc, o));
+      bad |= __shfl_xor_sync(FS_FULL, bad, o);
+    }
+    // max(l) * max(c) bounds every l * c: a conservative exactness guard
+    const int64_t mlc = (int64_t)ml * mc, sne = sall - seq;
+    if (b < nb && j == 0)
+      c2_finish(b, d, sq, skv, seq, sne, mlc, bad, o0, o1, q, kv, prm, h, out, status);
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)kC2Stages * gridDim.x;
+      if (tn < n_tiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads -> TMA writes
+        c2_issue(S, st, tn, nb, q, kv, off, aligned);
+      }
+    }
   }
 }
 
@@ -253,7 +422,28 @@ int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* of
                           int32_t* status, int n_sms, void* stream) {
   if (nb <= 0) return 0;
   const int threads = 256;
-  if (getenv("FS_C2_WARP") == nullptr) {
+  // "tpb" (default: 167 us for 2^20 x 72-request batches), "tma" (313 us: DRAM reads
+  // exactly the algorithmic bytes but 8 warps/SM leave it latency bound), "warp"
+  const char* mode = getenv("FS_C2");
+  if (mode != nullptr && strcmp(mode, "tma") == 0) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(attention_cost_kernel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(C2Smem));
+      configured = true;
+    }
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attention_cost_kernel_tma, kC2Threads,
+                                                  sizeof(C2Smem));
+    if (per < 1) per = 1;
+    const int64_t tiles = (nb + kC2TileBatches - 1) / kC2TileBatches;
+    int64_t blocks = (int64_t)n_sms * per;
+    if (blocks > tiles) blocks = tiles;
+    attention_cost_kernel_tma<<<(int)blocks, kC2Threads, sizeof(C2Smem), (cudaStream_t)stream>>>(
+        q, kv, off, dec, nb, prm, out, status);
+    return 1;
+  }
+  if (mode == nullptr || strcmp(mode, "warp") != 0) {
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attention_cost_kernel_tpb, threads, 0);
     if (per < 1) per = 1;

@@ -117,6 +117,32 @@ def test_attention_cost_bulk_vs_oracle(engine):
         assert out[b] == oracle.attention_us(bool(dec[b]), q[s:e], kv[s:e], 32, 8, 128, 2.25e15, 8e12)
 
 
+@pytest.mark.parametrize("mode", ["tpb", "tma", "warp"])
+def test_attention_cost_kernel_variants_agree(engine, mode, monkeypatch):
+    """Every C2 kernel variant (FS_C2) gives the default's bits, incl. ragged,
+    empty and invalid batches and an unaligned CSR start."""
+    from paper_2508_03148_b200.engine import attn_params
+    rs = np.random.default_rng(5)
+    lens = rs.integers(0, 300, size=3000)
+    lens[::97] = 0                                   # empty batches
+    off = np.concatenate([[3], 3 + np.cumsum(lens)]).astype(np.int64)  # unaligned start
+    n = int(off[-1])
+    kv = np.clip(rs.lognormal(6.5, 1.4, size=n), 1, 32768).astype(np.int32)
+    dec = (np.arange(3000) % 2).astype(np.uint8)
+    q = kv.copy()
+    for b in range(3000):
+        if dec[b]:
+            q[off[b]:off[b + 1]] = 1
+    q[off[500]] = 0                                   # invalid member
+    p = attn_params(32, 8, 128, 2, 2.25e15, 8e12, 5.0)
+    monkeypatch.delenv("FS_C2", raising=False)
+    want, wst = engine.attention_cost(q, kv, off, dec, p)
+    monkeypatch.setenv("FS_C2", mode)
+    got, gst = engine.attention_cost(q, kv, off, dec, p)
+    assert (gst == wst).all()
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
 def test_sweep_driver_end_to_end(engine, tmp_path):
     """run_sweep on the GPU: ok rows equal the oracle's metrics, failures become rows."""
     import csv
