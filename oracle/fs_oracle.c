@@ -1768,6 +1768,11 @@ double fso_attention_us(int decode, const int64_t* q, const int64_t* kv, int B, 
   fs_cost_ctx c = {peak, bw, ovh, 1, 1, 1, 1};
   return attention_us_analytic(decode, q, kv, B, hq, hkv, hdim, &c, dt);
 }
+/* topology.collective_time(kind, bytes_per_rank, n, link) (topology.py:370-394);
+ * kind 0 all_to_all, 1 all_reduce, 2 all_gather */
+double fso_collective(int kind, double bytes_per_rank, int n, double lat, double bw) {
+  return collective_flt(kind, bytes_per_rank, n, lat, bw);
+}
 double fso_linear_us(int64_t m, int64_t n, int64_t k, double peak, double bw, double ovh, int dt) {
   fs_cost_ctx c = {peak, bw, ovh, 1, 1, 1, 1};
   return linear_us(m, n, k, &c, dt);

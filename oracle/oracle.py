@@ -52,6 +52,9 @@ def load():
                               ctypes.c_double, ctypes.c_uint64, vp]
     lib.fso_dirichlet_row.restype = None
     lib.fso_dirichlet_row.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, vp, vp]
+    lib.fso_collective.restype = ctypes.c_double
+    lib.fso_collective.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                   ctypes.c_double]
     lib.fso_gg_features.restype = ctypes.c_double
     lib.fso_gg_features.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int, vp]

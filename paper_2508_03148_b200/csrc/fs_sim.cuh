@@ -52,6 +52,22 @@
 #ifndef FS_ROW8_FAST  // straight-line routing pass for whole 8-draw row segments
 #define FS_ROW8_FAST 0
 #endif
+#ifndef FS_PHILOX_PEEL  // first two Philox rounds specialised (counter < 2^32, c2 = 0)
+#define FS_PHILOX_PEEL 0
+#endif
+#ifndef FS_OUTLINE  // DES handlers out of line: 1 = prefill/PD/AF/log paths, 2 = + decode path
+#define FS_OUTLINE 0
+#endif
+#if FS_OUTLINE >= 1
+#define FS_OUT1 __device__ __noinline__
+#else
+#define FS_OUT1 __device__
+#endif
+#if FS_OUTLINE >= 2
+#define FS_OUT2 __device__ __noinline__
+#else
+#define FS_OUT2 __device__
+#endif
 #ifndef FS_COLD_NOINLINE  // rare routing paths out of line (compact hot code)
 #define FS_COLD_NOINLINE 0
 #endif
@@ -127,7 +143,7 @@ __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, 
 __device__ __forceinline__ bool hev_less(const HEv& a, const HEv& b) {
   return a.t < b.t || (a.t == b.t && a.seq < b.seq);
 }
-__device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
+FS_OUT2 void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   if (t < I.now) { fail(I, FS_ERR_SCHEDULING_IN_PAST, kind); return; }
   __syncwarp();
   if (I.lane == 0) {
@@ -147,7 +163,7 @@ __device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   I.seq++;
   __syncwarp();
 }
-__device__ HEv heap_pop(Inst& I) {
+FS_OUT2 HEv heap_pop(Inst& I) {
   HEv top;
   top.t = 0; top.seq = 0; top.kind = 0; top.a = 0; top.b = 0;
   __syncwarp();
@@ -301,7 +317,7 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
   return policy == FS_ROUTE_DIRICHLET ? FS_ERR_INTERNAL : FS_ERR_ROUTING;
 }
 
-__device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
+FS_OUT1 void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
                           int64_t T, const WarpSmem* sm) {
   if (!P.log_enabled || !P.log.routes) return;
   const int E = I.d->num_experts;
@@ -471,6 +487,15 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
     if (b + 1 <= blast) consume(B, b + 1);
   }
 #else
+#if FS_PHILOX_PEEL
+  if (((n1 - 1) >> 2) + 1 < (1ull << 32)) {
+    const uint64_t pm_hi = __umul64hi(0xD2E7470EE14C6C93ull, k0);
+    const uint64_t pm_lo = 0xD2E7470EE14C6C93ull * k0;
+    for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++)
+      consume(philox4x64_10_peeled((uint32_t)(b + 1), k0, k1, pm_hi, pm_lo), b);
+    return;
+  }
+#endif
   for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) consume(philox4x64_10(b + 1, k0, k1), b);
 #endif
 }
@@ -964,7 +989,7 @@ __device__ __noinline__ int learned_moe_layer_warp(const EngineParams& P, Inst& 
 
 // Duration in us (same on all lanes). moe_out (global) receives per-layer raw
 // moe_imbalance ratios when non-null.
-__device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
+FS_OUT2 double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
                                 const BatchShape& b, int64_t step, WarpSmem* sm,
                                 double* moe_out) {
   const fs_instance_desc* d = I.d;
@@ -1058,14 +1083,14 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
 // A batch's moe-ratio slot is reserved when it starts: several replicas can have
 // batches in flight, so slots are handed out in start order and each batch
 // record points at its own. Returns offset + 1 (0 = not logged).
-__device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
+FS_OUT1 int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
   if (!P.log_enabled || !P.log.batches || !I.d->has_moe) return 0;
   if (I.log_eoff + I.d->num_layers > P.log.moe_cap) return 0;
   const int32_t off = I.log_eoff;
   I.log_eoff += I.d->num_layers;
   return off + 1;
 }
-__device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
+FS_OUT1 void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
                           const int32_t* members, int nm, int32_t moe_off1) {
   if (!P.log_enabled || !P.log.batches) return;
   const int n_moe = moe_off1 ? I.d->num_layers : 0;
@@ -1128,7 +1153,7 @@ __device__ __forceinline__ bool prio_less(const EngineParams& P, const Inst& I, 
 }
 
 // enqueue a waiting request; priority admission keeps the queue in key order
-__device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
+FS_OUT1 void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
   int32_t* q = qlist(I, r);
   if (I.d->admission == FS_ADMIT_PRIORITY) {
     int pos = 0;
@@ -1163,7 +1188,7 @@ struct Admit {
 };
 
 // Admitted members (candidate order) go to the inflight list and leave the queue.
-__device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
+FS_OUT1 Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
                                int running_count, int64_t capacity) {
   const fs_instance_desc* d = I.d;
   int32_t* q = qlist(I, r);
@@ -1248,7 +1273,7 @@ __device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& 
 }
 
 // ---- batch launch helpers ----------------------------------------------------------------------
-__device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
+FS_OUT2 void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, const BatchShape& b, int phase,
                              WarpSmem* sm) {
   const int32_t moe_off1 = log_moe_reserve(P, I);
@@ -1264,7 +1289,7 @@ __device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
 }
 
-__device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
+FS_OUT1 void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
                               const fs_replica_desc& rd, const Admit& A, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -1301,7 +1326,7 @@ __device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s
   launch_batch(P, I, r, s, rd, b, PH_PREFILL, sm);
 }
 
-__device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
+FS_OUT2 void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -1327,7 +1352,7 @@ __device__ void kick(Inst& I, int r, RepState& s) {
 }
 
 // append requests (cooperatively: lane i holds req if has) to the running list
-__device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
+FS_OUT2 void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
                                int req, int emitted) {
   const unsigned lt = (1u << I.lane) - 1u;
   const unsigned hm = __ballot_sync(FS_FULL, has);
@@ -1349,7 +1374,7 @@ __device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& 
 
 // prefill completion (colocated.py:70-91, pd.py:98-112, af.py:514-535).
 // to_running: co-located / AF; otherwise PD (unfinished go to the transfer FIFO).
-__device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
+FS_OUT1 void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
                                  bool to_running) {
   const fs_instance_desc* d = I.d;
   const int32_t* il = ilist(I, r);
@@ -1389,7 +1414,7 @@ __device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState
 // decode / AF completion: every member emitted one token; finished requests leave
 // the running list in order (colocated.py:92-107, pd.py:113-127, af.py:536-551).
 // Returns the number finished. pool charge per finished request = rounded(prompt+output).
-__device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
+FS_OUT2 int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // TOKEN_EMITTED
   s.dstep++;
@@ -1432,7 +1457,7 @@ __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& 
 }
 
 // ---- co-located (colocated.py) ------------------------------------------------------------------
-__device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
+FS_OUT1 void co_arrival(const EngineParams& P, Inst& I, int req) {
   const int r = I.rr % I.R;
   I.rr++;
   RepState s = load_rep(P, I, r);
@@ -1441,10 +1466,10 @@ __device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   store_rep(P, I, r, s);
 }
 
-__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+FS_OUT1 void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm);
 
-__device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+FS_OUT2 void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
   if (!s.busy) {
@@ -1463,7 +1488,7 @@ __device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* 
   store_rep(P, I, r, s);
 }
 
-__device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+FS_OUT2 void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1482,7 +1507,7 @@ __device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t
 
 // ---- PD (pd.py) ---------------------------------------------------------------------------------
 // argmin over replicas of `role` by (key value, key_rank); value from rstate
-__device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
+FS_OUT1 int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
   int64_t best_v = INT64_MAX;
   int best_rank = 0x7fffffff, best_r = -1;
   for (int r = I.lane; r < I.R; r += 32) {
@@ -1504,7 +1529,7 @@ __device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_u
   return best_r;
 }
 
-__device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
+FS_OUT1 void pd_arrival(const EngineParams& P, Inst& I, int req) {
   __syncwarp();
   const int r = pd_pick(P, I, FS_ROLE_PREFILL, false);
   RepState s = load_rep(P, I, r);
@@ -1516,7 +1541,7 @@ __device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
 }
 
 // _pump_transfers (pd.py:141-192): strict FIFO, decode replica by (used, key)
-__device__ void pd_pump(const EngineParams& P, Inst& I) {
+FS_OUT1 void pd_pump(const EngineParams& P, Inst& I) {
   const fs_instance_desc* d = I.d;
   while (I.xt > I.xh && I.status == FS_OK) {
     const int req = P.xfer[I.ro + I.xh % I.N];
@@ -1537,7 +1562,7 @@ __device__ void pd_pump(const EngineParams& P, Inst& I) {
   }
 }
 
-__device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+FS_OUT1 void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
@@ -1569,7 +1594,7 @@ __device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* 
   store_rep(P, I, r, s);
 }
 
-__device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+FS_OUT1 void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1591,7 +1616,7 @@ __device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t
   store_rep(P, I, r, s);
 }
 
-__device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
+FS_OUT1 void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // MEMORY_AVAILABLE
   __syncwarp();
@@ -1613,7 +1638,7 @@ __device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req
 }
 
 // ---- AF step (af.py:244-319, 468-507) ------------------------------------------------------------
-__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+FS_OUT1 void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   const int L = d->num_layers;

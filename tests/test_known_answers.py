@@ -1,0 +1,65 @@
+"""Known-answer values the reference's own tests pin,
+checked against this repo's host mirror, the C oracle and -- where the value is
+on the device path -- the CUDA engine.
+
+Reference tests: test_analytic.py:31-36 (linear FLOP term), test_topology.py:
+107-110 (KV bytes/token), 135-138 (ring all-reduce), test_routing_moe.py:28-30
+(top_k == E saturation), test_core.py:166-169 (ns rounding half to even).
+"""
+
+import numpy as np
+import pytest
+
+from paper_2508_03148_b200.topology import ModelConfig, kv_bytes_per_token
+
+
+def test_linear_flop_term_hand_value():
+    from oracle import oracle
+    lib = oracle.load()
+    peak, bw, ovh = 312e12, 2.0e12, 5.0
+    t = lib.fso_linear_us(1024, 4096, 4096, peak, bw, ovh, 2)
+    flop_term_us = 2 * 1024 * 4096 * 4096 / 312e12 * 1e6
+    assert flop_term_us == pytest.approx(110.1, abs=0.1)
+    assert t == pytest.approx(ovh + flop_term_us, rel=1e-6)
+
+
+def test_kv_bytes_per_token_hand_arithmetic():
+    m = ModelConfig(num_layers=28, d_model=3584, d_ff=18944, num_query_heads=28,
+                    num_kv_heads=4, head_dim=128, dtype_bytes=2)
+    assert kv_bytes_per_token(m) == 57_344
+    unit = ModelConfig(num_layers=1, d_model=1, d_ff=1, num_query_heads=1, num_kv_heads=1,
+                       head_dim=1, dtype_bytes=2)
+    assert kv_bytes_per_token(unit) == 4
+
+
+def test_collectives_hand_values():
+    from oracle import oracle
+    lib = oracle.load()
+    # 2*alpha + 2*(1 MB * 1/2)/beta = 10 us + 10 us
+    assert lib.fso_collective(1, 1e6, 2, 5e-6, 100e9) == pytest.approx(20e-6)
+    for kind in (0, 1, 2):
+        assert lib.fso_collective(kind, 1e6, 1, 5e-6, 100e9) == 0.0
+    assert lib.fso_collective(0, 1e6, 4, 5e-6, 100e9) < lib.fso_collective(1, 1e6, 4, 5e-6, 100e9)
+
+
+def test_topk_equals_e_saturates_oracle():
+    from oracle import oracle
+    for policy in ("uniform", "dirichlet_skew"):
+        c, st = oracle.route(37, 8, 8, policy, 5)
+        assert st == 0 and c == [37] * 8
+
+
+@pytest.mark.gpu
+def test_topk_equals_e_saturates_device(engine):
+    for policy in ("uniform", "dirichlet_skew"):
+        counts, st = engine.route_tokens([37, 0, 5], [5, 6, 7], 8, 8, policy)
+        assert (st == 0).all()
+        assert counts.tolist() == [[37] * 8, [0] * 8, [5] * 8]
+
+
+@pytest.mark.gpu
+def test_invalid_topk_and_alpha_on_device(engine):
+    _, st = engine.route_tokens([10], [1], 8, 9, "uniform")
+    assert st.tolist() == [8]  # FS_ERR_INVALID_TOPK (routing.py:76-77)
+    _, st = engine.route_tokens([10], [1], 8, 2, "dirichlet_skew", 0.0)
+    assert st.tolist() == [5]  # RoutingError: dirichlet_skew needs alpha > 0
