@@ -301,37 +301,6 @@ __device__ __forceinline__ U4 philox4x64_10(uint64_t c0, uint64_t k0, uint64_t k
   return o;
 }
 
-// The same block for a counter (c0 < 2^32, 0, 0, 0) with the first two rounds
-// peeled: round 1 multiplies M1 by c2 = 0, and round 2's M0 operand is round 1's
-// n0 = k0 -- the same for every block of a key -- so pm = M0 * k0 (hi, lo) is
-// computed once per key by the caller. Rounds 3..10 run the rolled loop.
-__device__ __forceinline__ U4 philox4x64_10_peeled(uint32_t c0, uint64_t k0, uint64_t k1,
-                                                   uint64_t pm_hi, uint64_t pm_lo) {
-  const uint64_t m0 = 0xD2E7470EE14C6C93ull, m1 = 0xCA5A826395121157ull;
-  // round 1 (keys k0, k1): c = (c0, 0, 0, 0)
-  const uint64_t p = (uint64_t)c0 * (uint32_t)m0;                 // 32 x 32 -> 64
-  const uint64_t q = (uint64_t)c0 * (uint32_t)(m0 >> 32) + (p >> 32);
-  const uint64_t r1_lo = (q << 32) | (uint32_t)p, r1_hi = q >> 32;  // M0 * c0 for c0 < 2^32
-  uint64_t x2 = r1_hi ^ k1;                                        // c2 after round 1
-  const uint64_t x3 = r1_lo;                                       // c3 after round 1
-  // round 2 (keys k0 + C0, k1 + C1): c0 = k0 (multiplied in advance), c1 = 0
-  k0 += 0x9E3779B97F4A7C15ull; k1 += 0xBB67AE8584CAA73Bull;
-  const uint64_t lo1 = m1 * x2, hi1 = __umul64hi(m1, x2);
-  uint64_t c0n = hi1 ^ k0, c1 = lo1, c2 = pm_hi ^ x3 ^ k1, c3 = pm_lo;
-  k0 += 0x9E3779B97F4A7C15ull; k1 += 0xBB67AE8584CAA73Bull;
-#pragma unroll kPhiloxUnroll
-  for (int r = 2; r < 10; r++) {
-    uint64_t lo0 = m0 * c0n, hi0 = __umul64hi(m0, c0n);
-    uint64_t lo1b = m1 * c2, hi1b = __umul64hi(m1, c2);
-    uint64_t n0 = hi1b ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0n = n0; c1 = lo1b; c2 = n2; c3 = lo0;
-    k0 += 0x9E3779B97F4A7C15ull; k1 += 0xBB67AE8584CAA73Bull;
-  }
-  U4 o;
-  o.v[0] = c0n; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
-  return o;
-}
-
 // Two independent blocks (counters ca, cb) with their rounds interleaved, so a
 // lane has two multiply chains in flight (Philox rounds are serially dependent).
 __device__ __forceinline__ void philox4x64_10_x2(uint64_t ca, uint64_t cb, uint64_t k0,

@@ -49,28 +49,6 @@
 #ifndef FS_DIR_IN_ANALYTIC
 #define FS_DIR_IN_ANALYTIC 0
 #endif
-#ifndef FS_ROW8_FAST  // straight-line routing pass for whole 8-draw row segments
-#define FS_ROW8_FAST 0
-#endif
-#ifndef FS_PHILOX_PEEL  // first two Philox rounds specialised (counter < 2^32, c2 = 0)
-#define FS_PHILOX_PEEL 0
-#endif
-#ifndef FS_OUTLINE  // DES handlers out of line: 1 = prefill/PD/AF/log paths, 2 = + decode path
-#define FS_OUTLINE 0
-#endif
-#if FS_OUTLINE >= 1
-#define FS_OUT1 __device__ __noinline__
-#else
-#define FS_OUT1 __device__
-#endif
-#if FS_OUTLINE >= 2
-#define FS_OUT2 __device__ __noinline__
-#else
-#define FS_OUT2 __device__
-#endif
-#ifndef FS_COLD_NOINLINE  // rare routing paths out of line (compact hot code)
-#define FS_COLD_NOINLINE 0
-#endif
 
 namespace fs {
 namespace FS_SIM_NS {
@@ -143,7 +121,7 @@ __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, 
 __device__ __forceinline__ bool hev_less(const HEv& a, const HEv& b) {
   return a.t < b.t || (a.t == b.t && a.seq < b.seq);
 }
-FS_OUT2 void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
+__device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   if (t < I.now) { fail(I, FS_ERR_SCHEDULING_IN_PAST, kind); return; }
   __syncwarp();
   if (I.lane == 0) {
@@ -163,7 +141,7 @@ FS_OUT2 void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   I.seq++;
   __syncwarp();
 }
-FS_OUT2 HEv heap_pop(Inst& I) {
+__device__ HEv heap_pop(Inst& I) {
   HEv top;
   top.t = 0; top.seq = 0; top.kind = 0; top.a = 0; top.b = 0;
   __syncwarp();
@@ -258,14 +236,6 @@ __device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int pref
   __syncwarp();
 }
 
-#if FS_COLD_NOINLINE
-// the owning-warp uniform router: only the RNG-free shortcuts and jobs the board
-// does not take reach it in a sweep, so it stays out of line
-__device__ __noinline__ int route_uniform_cold(int lane, int64_t T, int E, int k, uint64_t k0,
-                                               uint64_t k1, int* counts) {
-  return route_uniform_warp(lane, T, E, k, k0, k1, counts);
-}
-#endif
 
 // keys a router call draws (T x E; none for the trace policy and the RNG-free shortcuts)
 __device__ __forceinline__ int64_t draws_of(const fs_instance_desc* d, int policy, int64_t T) {
@@ -301,11 +271,7 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
   if (T == 0 || k == E || policy == FS_ROUTE_UNIFORM) {
     if (T > 0 && k < E && k > FS_MAX_TOPK) return FS_ERR_CAPACITY;
     __syncwarp();
-#if FS_COLD_NOINLINE
-    return route_uniform_cold(I.lane, T, E, k, k0, k1, sm->counts);
-#else
     return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
-#endif
   }
 #if FS_LEARNED || FS_DIR_IN_ANALYTIC
   // dirichlet_skew instances run in the extended (learned) variant of this kernel:
@@ -317,7 +283,7 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
   return policy == FS_ROUTE_DIRICHLET ? FS_ERR_INTERNAL : FS_ERR_ROUTING;
 }
 
-FS_OUT1 void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
+__device__ void log_route(const EngineParams& P, Inst& I, int r, int mb, int64_t step, int layer,
                           int64_t T, const WarpSmem* sm) {
   if (!P.log_enabled || !P.log.routes) return;
   const int E = I.d->num_experts;
@@ -442,41 +408,6 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
       }
     }
   };
-#if FS_ROW8_FAST
-  if (((n0 | n1) & 7) == 0) {
-    // the row segment is whole 8-draw groups (E a multiple of 8, one segment
-    // per row): block pairs, no range predicates, two blocks in flight
-    for (uint64_t b = n0 >> 2; b < (n1 >> 2); b += 2) {
-      U4 A, B;
-#if FS_ROW8_FAST >= 2
-      philox4x64_10_x2(b + 1, b + 2, k0, k1, A, B);
-#else
-      A = philox4x64_10(b + 1, k0, k1);
-      B = philox4x64_10(b + 2, k0, k1);
-#endif
-      const uint32_t eb0 = (uint32_t)(4 * b - rb);
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const uint64_t w = j < 4 ? A.v[j] : B.v[j - 4];
-        uint32_t x = ((uint32_t)(w >> 32) & ~emask) | (eb0 + (uint32_t)j);
-        if (KCAP <= 4 || x < thr) {
-#pragma unroll
-          for (int q = 0; q < KCAP; q++) {
-            const uint32_t lo = min(top[q], x);
-            x = max(top[q], x);
-            top[q] = lo;
-          }
-          if (KCAP > 4) {
-#pragma unroll
-            for (int q = 0; q < KCAP; q++)
-              if (q == kc - 1) thr = top[q];
-          }
-        }
-      }
-    }
-    return;
-  }
-#endif
 #if FS_PHILOX_ILP >= 2
   // two blocks per step (a trailing odd block is generated and ignored)
   const uint64_t blast = (n1 - 1) >> 2;
@@ -487,49 +418,10 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
     if (b + 1 <= blast) consume(B, b + 1);
   }
 #else
-#if FS_PHILOX_PEEL
-  if (((n1 - 1) >> 2) + 1 < (1ull << 32)) {
-    const uint64_t pm_hi = __umul64hi(0xD2E7470EE14C6C93ull, k0);
-    const uint64_t pm_lo = 0xD2E7470EE14C6C93ull * k0;
-    for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++)
-      consume(philox4x64_10_peeled((uint32_t)(b + 1), k0, k1, pm_hi, pm_lo), b);
-    return;
-  }
-#endif
   for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) consume(philox4x64_10(b + 1, k0, k1), b);
 #endif
 }
 
-#if FS_COLD_NOINLINE
-// Exact 64-bit redo of one pass (the 32-bit surrogate keys tied at the k-th /
-// (k+1)-th boundary): rare, so out of line to keep the hot loop's code compact.
-// Fills ids[] and returns 1 on a true boundary tie.
-template <int KCAP>
-__device__ __noinline__ int exact_redo(int (&ids)[KCAP], bool active, bool leader, int e0, int e1,
-                                       uint64_t rb, int nseg, int k, uint64_t k0, uint64_t k1) {
-  const int kc = k + 1;
-  uint64_t t64[KCAP];
-#pragma unroll
-  for (int j = 0; j < KCAP; j++) t64[j] = ~0ull;
-  uint64_t thr = ~0ull;
-  if (active && e0 < e1) topk_scan<KCAP>(t64, kc, thr, rb + e0, rb + e1, rb, k0, k1);
-  for (int s = 1; s < nseg; s <<= 1) {
-    uint64_t other[KCAP];
-#pragma unroll
-    for (int j = 0; j < KCAP; j++) other[j] = __shfl_xor_sync(FS_FULL, t64[j], s);
-#pragma unroll
-    for (int j = 0; j < KCAP; j++)
-      if (j < kc) topk_insert<KCAP>(t64, kc, other[j], thr);
-  }
-  int tie = 0;
-#pragma unroll
-  for (int j = 0; j < KCAP; j++) {
-    ids[j] = (int)(t64[j] & 0x7FF);
-    if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
-  }
-  return tie;
-}
-#endif
 
 template <int KCAP>
 __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
@@ -599,9 +491,6 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
 #pragma unroll
     for (int j = 0; j < KCAP; j++) ids[j] = (int)(top[j] & emask);
     if (__any_sync(FS_FULL, unsure)) {
-#if FS_COLD_NOINLINE
-      tie |= exact_redo<KCAP>(ids, active, leader, e0, e1, rb, nseg, k, k0, k1);
-#else
       // exact 64-bit redo of this pass
       uint64_t t64[KCAP];
 #pragma unroll
@@ -621,7 +510,6 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
         ids[j] = (int)(t64[j] & 0x7FF);
         if (j == k && leader && ((t64[j] >> 11) == (t64[j > 0 ? j - 1 : 0] >> 11))) tie = 1;
       }
-#endif
     }
     if (local) {
       if (leader) {
@@ -989,7 +877,7 @@ __device__ __noinline__ int learned_moe_layer_warp(const EngineParams& P, Inst& 
 
 // Duration in us (same on all lanes). moe_out (global) receives per-layer raw
 // moe_imbalance ratios when non-null.
-FS_OUT2 double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
+__device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
                                 const BatchShape& b, int64_t step, WarpSmem* sm,
                                 double* moe_out) {
   const fs_instance_desc* d = I.d;
@@ -1083,14 +971,14 @@ FS_OUT2 double execute_batch(const EngineParams& P, Inst& I, int r, const fs_rep
 // A batch's moe-ratio slot is reserved when it starts: several replicas can have
 // batches in flight, so slots are handed out in start order and each batch
 // record points at its own. Returns offset + 1 (0 = not logged).
-FS_OUT1 int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
+__device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
   if (!P.log_enabled || !P.log.batches || !I.d->has_moe) return 0;
   if (I.log_eoff + I.d->num_layers > P.log.moe_cap) return 0;
   const int32_t off = I.log_eoff;
   I.log_eoff += I.d->num_layers;
   return off + 1;
 }
-FS_OUT1 void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
+__device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
                           const int32_t* members, int nm, int32_t moe_off1) {
   if (!P.log_enabled || !P.log.batches) return;
   const int n_moe = moe_off1 ? I.d->num_layers : 0;
@@ -1153,7 +1041,7 @@ __device__ __forceinline__ bool prio_less(const EngineParams& P, const Inst& I, 
 }
 
 // enqueue a waiting request; priority admission keeps the queue in key order
-FS_OUT1 void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
+__device__ void enqueue(const EngineParams& P, Inst& I, int r, RepState& s, int req) {
   int32_t* q = qlist(I, r);
   if (I.d->admission == FS_ADMIT_PRIORITY) {
     int pos = 0;
@@ -1188,7 +1076,7 @@ struct Admit {
 };
 
 // Admitted members (candidate order) go to the inflight list and leave the queue.
-FS_OUT1 Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
+__device__ Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, bool full,
                                int running_count, int64_t capacity) {
   const fs_instance_desc* d = I.d;
   int32_t* q = qlist(I, r);
@@ -1273,7 +1161,7 @@ FS_OUT1 Admit admit_prefill(const EngineParams& P, Inst& I, int r, RepState& s, 
 }
 
 // ---- batch launch helpers ----------------------------------------------------------------------
-FS_OUT2 void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, const BatchShape& b, int phase,
                              WarpSmem* sm) {
   const int32_t moe_off1 = log_moe_reserve(P, I);
@@ -1289,7 +1177,7 @@ FS_OUT2 void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
 }
 
-FS_OUT1 void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
                               const fs_replica_desc& rd, const Admit& A, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -1326,7 +1214,7 @@ FS_OUT1 void start_prefill(const EngineParams& P, Inst& I, int r, RepState& s,
   launch_batch(P, I, r, s, rd, b, PH_PREFILL, sm);
 }
 
-FS_OUT2 void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
                              const fs_replica_desc& rd, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   BatchShape b;
@@ -1352,7 +1240,7 @@ __device__ void kick(Inst& I, int r, RepState& s) {
 }
 
 // append requests (cooperatively: lane i holds req if has) to the running list
-FS_OUT2 void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
+__device__ void running_append(const EngineParams& P, Inst& I, int r, RepState& s, bool has,
                                int req, int emitted) {
   const unsigned lt = (1u << I.lane) - 1u;
   const unsigned hm = __ballot_sync(FS_FULL, has);
@@ -1374,7 +1262,7 @@ FS_OUT2 void running_append(const EngineParams& P, Inst& I, int r, RepState& s, 
 
 // prefill completion (colocated.py:70-91, pd.py:98-112, af.py:514-535).
 // to_running: co-located / AF; otherwise PD (unfinished go to the transfer FIFO).
-FS_OUT1 void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
+__device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s,
                                  bool to_running) {
   const fs_instance_desc* d = I.d;
   const int32_t* il = ilist(I, r);
@@ -1414,7 +1302,7 @@ FS_OUT1 void prefill_complete(const EngineParams& P, Inst& I, int r, RepState& s
 // decode / AF completion: every member emitted one token; finished requests leave
 // the running list in order (colocated.py:92-107, pd.py:113-127, af.py:536-551).
 // Returns the number finished. pool charge per finished request = rounded(prompt+output).
-FS_OUT2 int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
+__device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // TOKEN_EMITTED
   s.dstep++;
@@ -1457,7 +1345,7 @@ FS_OUT2 int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) 
 }
 
 // ---- co-located (colocated.py) ------------------------------------------------------------------
-FS_OUT1 void co_arrival(const EngineParams& P, Inst& I, int req) {
+__device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   const int r = I.rr % I.R;
   I.rr++;
   RepState s = load_rep(P, I, r);
@@ -1466,10 +1354,10 @@ FS_OUT1 void co_arrival(const EngineParams& P, Inst& I, int req) {
   store_rep(P, I, r, s);
 }
 
-FS_OUT1 void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm);
 
-FS_OUT2 void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+__device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
   if (!s.busy) {
@@ -1488,7 +1376,7 @@ FS_OUT2 void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm)
   store_rep(P, I, r, s);
 }
 
-FS_OUT2 void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+__device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1507,7 +1395,7 @@ FS_OUT2 void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t du
 
 // ---- PD (pd.py) ---------------------------------------------------------------------------------
 // argmin over replicas of `role` by (key value, key_rank); value from rstate
-FS_OUT1 int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
+__device__ int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used) {
   int64_t best_v = INT64_MAX;
   int best_rank = 0x7fffffff, best_r = -1;
   for (int r = I.lane; r < I.R; r += 32) {
@@ -1529,7 +1417,7 @@ FS_OUT1 int pd_pick(const EngineParams& P, const Inst& I, int role, bool by_used
   return best_r;
 }
 
-FS_OUT1 void pd_arrival(const EngineParams& P, Inst& I, int req) {
+__device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
   __syncwarp();
   const int r = pd_pick(P, I, FS_ROLE_PREFILL, false);
   RepState s = load_rep(P, I, r);
@@ -1541,7 +1429,7 @@ FS_OUT1 void pd_arrival(const EngineParams& P, Inst& I, int req) {
 }
 
 // _pump_transfers (pd.py:141-192): strict FIFO, decode replica by (used, key)
-FS_OUT1 void pd_pump(const EngineParams& P, Inst& I) {
+__device__ void pd_pump(const EngineParams& P, Inst& I) {
   const fs_instance_desc* d = I.d;
   while (I.xt > I.xh && I.status == FS_OK) {
     const int req = P.xfer[I.ro + I.xh % I.N];
@@ -1562,7 +1450,7 @@ FS_OUT1 void pd_pump(const EngineParams& P, Inst& I) {
   }
 }
 
-FS_OUT1 void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
+__device__ void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   RepState s = load_rep(P, I, r);
   s.start_pending = 0;
@@ -1594,7 +1482,7 @@ FS_OUT1 void pd_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* sm)
   store_rep(P, I, r, s);
 }
 
-FS_OUT1 void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
+__device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t dur) {
   RepState s = load_rep(P, I, r);
   s.busy = 0;
   s.busy_ns += dur;
@@ -1616,7 +1504,7 @@ FS_OUT1 void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t du
   store_rep(P, I, r, s);
 }
 
-FS_OUT1 void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
+__device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // MEMORY_AVAILABLE
   __syncwarp();
@@ -1638,7 +1526,7 @@ FS_OUT1 void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req) {
 }
 
 // ---- AF step (af.py:244-319, 468-507) ------------------------------------------------------------
-FS_OUT1 void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
+__device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const fs_replica_desc& rd,
                               WarpSmem* sm) {
   const fs_instance_desc* d = I.d;
   const int L = d->num_layers;
