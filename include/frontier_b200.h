@@ -218,6 +218,28 @@ typedef struct {
   int64_t steps_executed;
 } fs_replica_out;
 
+/* Synthetic workload of one instance (workload.py:131-216 WorkloadSpec):
+ * arrivals and lengths drawn from numpy's Philox streams
+ * Generator(Philox(key=SeedSequence([seed, stream]).generate_state(2))) with
+ * stream 0 arrival, 1 prompt, 2 output (workload.py:36,188-190). */
+enum fs_arrival_kind { FS_ARRIVAL_POISSON = 0, FS_ARRIVAL_FIXED = 1, FS_ARRIVAL_AT_ZERO = 2 };
+enum fs_length_kind { FS_LEN_FIXED = 0, FS_LEN_UNIFORM = 1, FS_LEN_LOGNORMAL = 2 };
+typedef struct {
+  int32_t kind;               /* enum fs_length_kind */
+  int32_t pad;
+  int64_t value, lo, hi;      /* fixed value; clamp / uniform bounds (inclusive) */
+  double mu, sigma;           /* lognormal parameters */
+} fs_length_dist;             /* 48 bytes */
+typedef struct {
+  uint64_t seed;              /* WorkloadSpec.seed */
+  int32_t n_requests;
+  int32_t arrival_kind;       /* enum fs_arrival_kind */
+  double rate_rps;            /* poisson */
+  int64_t gap_ns;             /* fixed_interval */
+  int64_t out_offset;         /* first slot of this instance in the output arrays */
+  fs_length_dist prompt, output;
+} fs_workload_desc;           /* 136 bytes */
+
 /* Optional per-request outputs (indexed like the request SoA). */
 typedef struct {
   int64_t* first_token_ns;    /* first TOKEN_EMITTED */
@@ -364,6 +386,16 @@ int fs_route_uniform(fs_engine* e, const int64_t* tokens, const uint64_t* seeds,
 int fs_route_tokens(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, int32_t n_calls,
                     int32_t num_experts, int32_t top_k, int32_t policy, double alpha,
                     int32_t* counts_out, int32_t* status);
+
+/* generate(spec) for n instances on the device (workload.py:193-216): requests in
+ * generation order, which is arrival order for every synthetic arrival kind
+ * (cumulative gaps are non-decreasing), so the arrays are the request SoA of
+ * fs_run_batch as they stand; id_rank = rank of "r{i}" in Python str order.
+ * Host buffers indexed by out_offset + i. status per instance (FS_ERR_VALUE for
+ * an unknown kind). */
+int fs_generate_workload(fs_engine* e, const fs_workload_desc* w, int32_t n,
+                         int64_t* arrival_ns, int32_t* prompt_tokens, int32_t* output_tokens,
+                         int32_t* id_rank, int32_t* status);
 
 /* derive_router_seed for (prefix, step, layer[, micro_batch]) tuples (host buffers). */
 int fs_router_seeds(fs_engine* e, const fs_seed_prefix* prefixes, const int32_t* prefix_idx,

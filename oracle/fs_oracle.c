@@ -1748,6 +1748,135 @@ int fso_route(int64_t T, int32_t E, int32_t k, int32_t policy, double alpha, uin
 int fso_route_uniform(int64_t T, int32_t E, int32_t k, uint64_t seed, int32_t* counts_out) {
   return fso_route(T, E, k, FS_ROUTE_UNIFORM, 0.3, seed, counts_out);
 }
+/* ---- synthetic workload (workload.py:131-216) ---- */
+/* numpy Philox next_uint32: low half of a 64-bit draw first, then the high half */
+typedef struct { np_philox g; int has32; uint32_t u32; } np_stream32;
+static uint32_t np_next_u32(np_stream32* s) {
+  if (s->has32) { s->has32 = 0; return s->u32; }
+  uint64_t v = np_next_u64(&s->g);
+  s->has32 = 1;
+  s->u32 = (uint32_t)(v >> 32);
+  return (uint32_t)v;
+}
+/* Generator.integers(lo, hi + 1, dtype=int64): random_bounded_uint64_fill, Lemire */
+static int64_t np_integer(np_stream32* s, int64_t lo, int64_t hi) {
+  uint64_t rng = (uint64_t)(hi - lo);
+  if (rng == 0) return lo;
+  if (rng <= 0xFFFFFFFFull) {
+    if (rng == 0xFFFFFFFFull) return lo + (int64_t)np_next_u32(s);
+    const uint32_t excl = (uint32_t)rng + 1u;
+    uint64_t m = (uint64_t)np_next_u32(s) * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+      const uint32_t thr = (uint32_t)(UINT32_MAX - (uint32_t)rng) % excl;
+      while (left < thr) { m = (uint64_t)np_next_u32(s) * excl; left = (uint32_t)m; }
+    }
+    return lo + (int64_t)(m >> 32);
+  }
+  if (rng == UINT64_MAX) return lo + (int64_t)np_next_u64(&s->g);
+  const uint64_t excl = rng + 1;
+  unsigned __int128 m = (unsigned __int128)np_next_u64(&s->g) * excl;
+  uint64_t left = (uint64_t)m;
+  if (left < excl) {
+    const uint64_t thr = (UINT64_MAX - rng) % excl;
+    while (left < thr) { m = (unsigned __int128)np_next_u64(&s->g) * excl; left = (uint64_t)m; }
+  }
+  return lo + (int64_t)(m >> 64);
+}
+/* key = SeedSequence([seed, stream]).generate_state(2, uint64) (workload.py:188-190) */
+static void workload_key(uint64_t seed, uint32_t stream, uint64_t key[2]) {
+  uint32_t ent[4], st[4];
+  int n = int_words(seed, ent);
+  n += int_words(stream, ent + n);
+  seedseq_state(ent, n, st, 4);
+  key[0] = (uint64_t)st[0] | ((uint64_t)st[1] << 32);
+  key[1] = (uint64_t)st[2] | ((uint64_t)st[3] << 32);
+}
+static int sample_lengths(const fs_length_dist* L, uint64_t seed, uint32_t stream, int n,
+                          int32_t* out) {
+  np_stream32 s;
+  memset(&s, 0, sizeof s);
+  workload_key(seed, stream, s.g.key);
+  for (int i = 0; i < n; i++) {
+    int64_t v;
+    if (L->kind == FS_LEN_FIXED) {
+      v = L->value;
+    } else if (L->kind == FS_LEN_UNIFORM) {
+      v = np_integer(&s, L->lo, L->hi);
+    } else if (L->kind == FS_LEN_LOGNORMAL) {
+      double x = rint(exp(L->mu + L->sigma * np_std_normal(&s.g)));  /* random_lognormal */
+      if (x < (double)L->lo) x = (double)L->lo;
+      if (x > (double)L->hi) x = (double)L->hi;
+      v = (int64_t)x;
+    } else {
+      return FS_ERR_VALUE;
+    }
+    out[i] = (int32_t)v;
+  }
+  return FS_OK;
+}
+/* Python str order rank of "r{i}" among "r0".."r{n-1}" */
+static int32_t id_str_rank(int64_t i, int64_t n) {
+  char t[24];
+  int m = sprintf(t, "%lld", (long long)i);
+  int64_t rank = 0, lo = 0, p10 = 1;
+  for (int d = 1; d <= 19 && lo < n; d++) {
+    const int64_t hi = (p10 > INT64_MAX / 10) ? INT64_MAX : p10 * 10;  /* [lo, hi) has d digits */
+    const int64_t end = hi < n ? hi : n;
+    if (d <= m) {
+      int64_t pre = 0;
+      for (int q = 0; q < d; q++) pre = pre * 10 + (t[q] - '0');
+      int64_t c = pre - lo; if (c < 0) c = 0; if (c > end - lo) c = end - lo;
+      rank += c;
+      if (d < m && pre >= lo && pre < end) rank += 1;   /* proper prefix sorts first */
+    } else {
+      int64_t scale = 1;
+      for (int q = 0; q < d - m; q++) scale *= 10;
+      int64_t tv = 0;
+      for (int q = 0; q < m; q++) tv = tv * 10 + (t[q] - '0');
+      /* d-digit j with floor(j / scale) < tv */
+      int64_t bound = tv * scale;               /* j < bound */
+      int64_t c = bound - lo; if (c < 0) c = 0; if (c > end - lo) c = end - lo;
+      rank += c;
+    }
+    lo = hi;
+    p10 = hi;
+    if (d == 1) lo = 10;
+  }
+  return (int32_t)rank;
+}
+int fso_generate_workload(const fs_workload_desc* w, int32_t n, int64_t* arrival_ns,
+                          int32_t* prompt, int32_t* output, int32_t* id_rank, int32_t* status) {
+  for (int k = 0; k < n; k++) {
+    const fs_workload_desc* d = &w[k];
+    const int64_t o = d->out_offset;
+    const int nr = d->n_requests;
+    int st = FS_OK;
+    if (d->arrival_kind == FS_ARRIVAL_POISSON) {
+      np_philox g;
+      memset(&g, 0, sizeof g);
+      workload_key(d->seed, 0, g.key);
+      const double scale = 1.0 / d->rate_rps;
+      double acc = 0.0;
+      for (int i = 0; i < nr; i++) {
+        acc = acc + scale * np_std_exponential(&g);   /* cumsum of exponential(scale) */
+        arrival_ns[o + i] = (int64_t)rint(acc * 1e9);
+      }
+    } else if (d->arrival_kind == FS_ARRIVAL_FIXED) {
+      for (int i = 0; i < nr; i++) arrival_ns[o + i] = (int64_t)i * d->gap_ns;
+    } else if (d->arrival_kind == FS_ARRIVAL_AT_ZERO) {
+      for (int i = 0; i < nr; i++) arrival_ns[o + i] = 0;
+    } else {
+      st = FS_ERR_VALUE;
+    }
+    if (!st) st = sample_lengths(&d->prompt, d->seed, 1, nr, prompt + o);
+    if (!st) st = sample_lengths(&d->output, d->seed, 2, nr, output + o);
+    for (int i = 0; i < nr; i++) id_rank[o + i] = id_str_rank(i, nr);
+    status[k] = st;
+  }
+  return 0;
+}
+
 /* GroupedGemmFeatures(..., mode="local").vector() and, with a forest set, the
  * learned prediction (features.py:166-209, model.py:323-326) */
 double fso_gg_features(const fs_forest_set* fs, int forest, const int64_t* counts, int n,
@@ -1795,7 +1924,8 @@ int fso_struct_sizes(int64_t* out, int n) {
                        (int64_t)sizeof(fs_replica_desc), (int64_t)sizeof(fs_instance_desc),
                        (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
                        (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
-                       (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc)};
+                       (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc),
+                       (int64_t)sizeof(fs_workload_desc)};
   const int k = (int)(sizeof(s) / sizeof(s[0]));
   for (int i = 0; i < n && i < k; i++) out[i] = s[i];
   return k;

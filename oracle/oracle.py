@@ -52,6 +52,8 @@ def load():
                               ctypes.c_double, ctypes.c_uint64, vp]
     lib.fso_dirichlet_row.restype = None
     lib.fso_dirichlet_row.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, vp, vp]
+    lib.fso_generate_workload.restype = ctypes.c_int
+    lib.fso_generate_workload.argtypes = [vp, ctypes.c_int32, vp, vp, vp, vp, vp]
     lib.fso_collective.restype = ctypes.c_double
     lib.fso_collective.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                    ctypes.c_double]
@@ -149,6 +151,20 @@ def gg_features(counts, d_model: int, d_ff: int, top_k: int, forests=None, fores
     v = load().fso_gg_features(ctypes.byref(fset) if fset is not None else None, forest,
                                abi.ptr(c), len(c), d_model, d_ff, top_k, abi.ptr(x))
     return x, v
+
+
+def generate_workload(descs):
+    """(arrival_ns, prompt, output, id_rank, status) for fs_workload_desc rows."""
+    descs = np.ascontiguousarray(descs, dtype=abi.WORKLOAD_DESC)
+    n_total = int((descs["out_offset"] + descs["n_requests"]).max()) if len(descs) else 0
+    arr = np.zeros(max(n_total, 1), np.int64)
+    pr = np.zeros(max(n_total, 1), np.int32)
+    out = np.zeros(max(n_total, 1), np.int32)
+    rk = np.zeros(max(n_total, 1), np.int32)
+    st = np.zeros(max(len(descs), 1), np.int32)
+    load().fso_generate_workload(abi.ptr(descs), len(descs), abi.ptr(arr), abi.ptr(pr),
+                                 abi.ptr(out), abi.ptr(rk), abi.ptr(st))
+    return arr[:n_total], pr[:n_total], out[:n_total], rk[:n_total], st[:len(descs)]
 
 
 def pysum(xs) -> float:

@@ -85,8 +85,16 @@ ATTN_PARAMS = np.dtype([("num_query_heads", "<i4"), ("num_kv_heads", "<i4"), ("h
 FOREST_DESC = np.dtype([("n_trees", "<i4"), ("n_features", "<i4"), ("tree_offset", "<i8")],
                        align=True)
 
+LENGTH_DIST = np.dtype([("kind", "<i4"), ("pad", "<i4"), ("value", "<i8"), ("lo", "<i8"),
+                        ("hi", "<i8"), ("mu", "<f8"), ("sigma", "<f8")], align=True)
+WORKLOAD_DESC = np.dtype([("seed", "<u8"), ("n_requests", "<i4"), ("arrival_kind", "<i4"),
+                          ("rate_rps", "<f8"), ("gap_ns", "<i8"), ("out_offset", "<i8"),
+                          ("prompt", LENGTH_DIST), ("output", LENGTH_DIST)], align=True)
+ARRIVAL_KINDS = {"poisson": 0, "fixed_interval": 1, "batch_at_zero": 2}
+LENGTH_KINDS = {"fixed": 0, "uniform": 1, "lognormal": 2}
+
 STRUCT_ORDER = (COST_CTX, SEED_PREFIX, REPLICA_DESC, INSTANCE_DESC, METRIC_ROW, REPLICA_OUT,
-                BATCH_REC, ROUTE_REC, ATTN_PARAMS, FOREST_DESC)
+                BATCH_REC, ROUTE_REC, ATTN_PARAMS, FOREST_DESC, WORKLOAD_DESC)
 
 
 class RequestSoA(ctypes.Structure):

@@ -10,6 +10,8 @@ the reference's per-point loop over `run_one` (cli.py:82-102, 197-237).
 from __future__ import annotations
 
 import time
+
+import numpy as np
 from dataclasses import dataclass
 
 from .config import DeploymentConfig, parse_config
@@ -30,12 +32,15 @@ class Failure:
         return f"failed: {type(self.exception).__name__}: {self.exception}"
 
 
-def instance_spec(config: DeploymentConfig) -> InstanceSpec:
-    """What `run_one` builds before `make_simulation` (cli.py:84-94)."""
+def instance_spec(config: DeploymentConfig, requests=None) -> InstanceSpec:
+    """What `run_one` builds before `make_simulation` (cli.py:84-94). `requests`
+    (RequestArrays) replaces the host generation when given (device_workload)."""
     attention_model, grouped_model = config.cost_model.load_models()
     check_model_slots_engine(attention_model, grouped_model)
     return InstanceSpec(
-        deployment=config.deployment(), requests=config.request_arrays(), policy=config.policy,
+        deployment=config.deployment(),
+        requests=requests if requests is not None else config.request_arrays(),
+        policy=config.policy,
         af=config.af if config.mode == "af" else None, routing=config.routing, seed=config.seed,
         attention_model=attention_model, grouped_gemm_model=grouped_model)
 
@@ -60,15 +65,63 @@ def run_specs(specs: list[InstanceSpec], engine: Engine | None = None,
     return BatchRun(low, split_results(low, raw, modes), t1 - t0, t2 - t1)
 
 
-def simulate(configs: list, engine: Engine | None = None, base_dir: str = "."
-             ) -> list[MetricsBundle | Failure]:
-    """Simulate every config on the GPU; per-instance errors become Failure entries."""
+def device_request_arrays(configs: list[DeploymentConfig], engine: Engine | None = None):
+    """Synthetic workloads of `configs` generated on the device in one call
+    (fs_generate_workload); None for configs that read a trace file. Raises the
+    reference's ValidationError for invalid distribution parameters, per config,
+    through the returned list (an Exception entry)."""
+    from .config import ValidationError
+    from .workload import RequestArrays, WorkloadError, workload_descs
+    eng = engine or default_engine()
+    out: list = [None] * len(configs)
+    idx, wl = [], []
+    for i, cfg in enumerate(configs):
+        if cfg.trace_path is not None:
+            continue
+        try:
+            workload_descs([cfg.workload])
+        except WorkloadError as exc:
+            out[i] = ValidationError(str(exc))
+            continue
+        idx.append(i)
+        wl.append(cfg.workload)
+    if wl:
+        descs = workload_descs(wl)
+        arr, pr, ou, _, st = eng.generate_workload(descs)
+        for j, i in enumerate(idx):
+            if st[j] != 0:
+                out[i] = ValidationError(f"workload generation failed (status {int(st[j])})")
+                continue
+            o, n = int(descs[j]["out_offset"]), int(descs[j]["n_requests"])
+            out[i] = RequestArrays([f"r{k}" for k in range(n)], arr[o:o + n].copy(),
+                                   pr[o:o + n].astype(np.int64), ou[o:o + n].astype(np.int64))
+    return out
+
+
+def simulate(configs: list, engine: Engine | None = None, base_dir: str = ".",
+             device_workload: bool = False) -> list[MetricsBundle | Failure]:
+    """Simulate every config on the GPU; per-instance errors become Failure entries.
+    device_workload: draw the synthetic request streams on the device too."""
     out: list[MetricsBundle | Failure | None] = [None] * len(configs)
     specs, where = [], []
+    parsed: list = [None] * len(configs)
     for i, c in enumerate(configs):
         try:
-            cfg = c if isinstance(c, DeploymentConfig) else parse_config(c, base_dir=base_dir)
-            specs.append(instance_spec(cfg))
+            parsed[i] = c if isinstance(c, DeploymentConfig) else parse_config(c, base_dir=base_dir)
+        except Exception as exc:  # config-time failures (cli.py:229-233)
+            out[i] = Failure(exc)
+    pre: list = [None] * len(configs)
+    if device_workload:
+        ok = [i for i in range(len(configs)) if parsed[i] is not None]
+        for i, r in zip(ok, device_request_arrays([parsed[i] for i in ok], engine)):
+            pre[i] = r
+    for i, cfg in enumerate(parsed):
+        if cfg is None:
+            continue
+        try:
+            if isinstance(pre[i], Exception):
+                raise pre[i]
+            specs.append(instance_spec(cfg, requests=pre[i]))
             where.append(i)
         except Exception as exc:  # config-time failures (cli.py:229-233)
             out[i] = Failure(exc)

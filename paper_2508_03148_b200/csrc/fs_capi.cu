@@ -55,6 +55,8 @@ struct fs_engine {
   // cost-model scratch
   DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
       c_layers, c_seeds, c_pf, c_mid, c_scratch;
+  // workload generation
+  DevBuf g_desc, g_arr, g_pr, g_out, g_rank, g_st;
   // learned models (persist across stages)
   DevBuf f_descs, f_roots, f_right, f_value, f_leaf;  // f_value: packed NodeP array
   fs::ForestView fv{};
@@ -96,7 +98,8 @@ int fs_struct_sizes(int64_t* out, int n) {
                        (int64_t)sizeof(fs_replica_desc), (int64_t)sizeof(fs_instance_desc),
                        (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
                        (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
-                       (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc)};
+                       (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc),
+                       (int64_t)sizeof(fs_workload_desc)};
   const int k = (int)(sizeof(s) / sizeof(s[0]));
   for (int i = 0; i < n && i < k; i++) out[i] = s[i];
   return k;
@@ -483,6 +486,44 @@ int fs_attention_features(fs_engine* e, const int32_t* q_lens, const int32_t* kv
                                      params, e->c_out.as<double>(), s);
   if (rc) return rc;
   FS_CHECK(cudaMemcpyAsync(out17, e->c_out.p, 17 * 8 * n_batches, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fs_generate_workload(fs_engine* e, const fs_workload_desc* w, int32_t n,
+                         int64_t* arrival_ns, int32_t* prompt_tokens, int32_t* output_tokens,
+                         int32_t* id_rank, int32_t* status) {
+  if (!e) return 1;
+  if (n < 0 || (n > 0 && !w)) { e->err = "fs_generate_workload: bad arguments"; return 13; }
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  int64_t total = 0;
+  for (int i = 0; i < n; i++) {
+    if (w[i].n_requests < 0 || w[i].out_offset < 0) {
+      e->err = "fs_generate_workload: negative size or offset";
+      return 13;
+    }
+    total = std::max(total, w[i].out_offset + w[i].n_requests);
+  }
+  FS_CHECK(upload(e->g_desc, w, (size_t)n, s));
+  FS_CHECK(e->g_arr.ensure((size_t)std::max<int64_t>(total, 1) * 8));
+  FS_CHECK(e->g_pr.ensure((size_t)std::max<int64_t>(total, 1) * 4));
+  FS_CHECK(e->g_out.ensure((size_t)std::max<int64_t>(total, 1) * 4));
+  FS_CHECK(e->g_rank.ensure((size_t)std::max<int64_t>(total, 1) * 4));
+  FS_CHECK(e->g_st.ensure((size_t)std::max(n, 1) * 4));
+  FS_CHECK(cudaMemsetAsync(e->g_st.p, 0, (size_t)std::max(n, 1) * 4, s));
+  e->last_launches = fs::launch_workload(e->g_desc.as<fs_workload_desc>(), n,
+                                         e->g_arr.as<int64_t>(), e->g_pr.as<int32_t>(),
+                                         e->g_out.as<int32_t>(), e->g_rank.as<int32_t>(),
+                                         e->g_st.as<int32_t>(), s);
+  FS_CHECK(cudaGetLastError());
+  if (total > 0) {
+    FS_CHECK(cudaMemcpyAsync(arrival_ns, e->g_arr.p, (size_t)total * 8, cudaMemcpyDeviceToHost, s));
+    FS_CHECK(cudaMemcpyAsync(prompt_tokens, e->g_pr.p, (size_t)total * 4, cudaMemcpyDeviceToHost, s));
+    FS_CHECK(cudaMemcpyAsync(output_tokens, e->g_out.p, (size_t)total * 4, cudaMemcpyDeviceToHost, s));
+    FS_CHECK(cudaMemcpyAsync(id_rank, e->g_rank.p, (size_t)total * 4, cudaMemcpyDeviceToHost, s));
+  }
+  if (n > 0) FS_CHECK(cudaMemcpyAsync(status, e->g_st.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
   FS_CHECK(cudaStreamSynchronize(s));
   return 0;
 }

@@ -417,6 +417,169 @@ __global__ void __launch_bounds__(kC2Threads) attention_cost_kernel_tma(
   }
 }
 
+// ---- synthetic workload generation (workload.py:131-216) --------------------------------------
+// One thread per (instance, stream): numpy's streams are sequential (variable
+// word consumption: ziggurat slow paths, Lemire rejections), so each stream is
+// one lane's loop; a sweep supplies thousands of instances x 3 streams.
+struct NpStream32 {
+  NpStream g;
+  int has32;
+  uint32_t u32;
+  __device__ uint32_t next_u32() {  // numpy Philox next_uint32: low half first
+    if (has32) { has32 = 0; return u32; }
+    const uint64_t v = g.next_u64();
+    has32 = 1;
+    u32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+  }
+};
+
+// Generator.integers(lo, hi + 1, dtype=int64): Lemire's bounded draw
+__device__ int64_t np_integer_dev(NpStream32& s, int64_t lo, int64_t hi) {
+  const uint64_t rng = (uint64_t)(hi - lo);
+  if (rng == 0) return lo;
+  if (rng <= 0xFFFFFFFFull) {
+    if (rng == 0xFFFFFFFFull) return lo + (int64_t)s.next_u32();
+    const uint32_t excl = (uint32_t)rng + 1u;
+    uint64_t m = (uint64_t)s.next_u32() * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+      const uint32_t thr = (0xFFFFFFFFu - (uint32_t)rng) % excl;
+      while (left < thr) { m = (uint64_t)s.next_u32() * excl; left = (uint32_t)m; }
+    }
+    return lo + (int64_t)(m >> 32);
+  }
+  if (rng == ~0ull) return lo + (int64_t)s.g.next_u64();
+  const uint64_t excl = rng + 1;
+  uint64_t x = s.g.next_u64();
+  uint64_t left = x * excl;
+  if (left < excl) {
+    const uint64_t thr = (~0ull - rng) % excl;
+    while (left < thr) { x = s.g.next_u64(); left = x * excl; }
+  }
+  return lo + (int64_t)__umul64hi(x, excl);
+}
+
+// key = SeedSequence([seed, stream]).generate_state(2, uint64) (workload.py:188-190)
+__device__ void workload_key_dev(uint64_t seed, uint32_t stream, uint64_t& k0, uint64_t& k1) {
+  uint32_t ent[4];
+  int n = int_words(seed, ent);
+  n += int_words(stream, ent + n);
+  uint64_t key[2];
+  seedseq_u64x2(ent, n, key);
+  k0 = key[0];
+  k1 = key[1];
+}
+
+__global__ void workload_kernel(const fs_workload_desc* __restrict__ w, int n,
+                                int64_t* __restrict__ arrival, int32_t* __restrict__ prompt,
+                                int32_t* __restrict__ output, int32_t* __restrict__ status) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 3 * n) return;
+  const int k = t / 3, which = t % 3;
+  const fs_workload_desc d = w[k];
+  const int64_t o = d.out_offset;
+  const int nr = d.n_requests;
+  NpStream32 s;
+  s.has32 = 0;
+  s.u32 = 0;
+  s.g.n = 0;
+  s.g.w0 = s.g.w1 = s.g.w2 = s.g.w3 = 0;
+  workload_key_dev(d.seed, (uint32_t)which, s.g.k0, s.g.k1);
+  if (which == 0) {
+    if (d.arrival_kind == FS_ARRIVAL_POISSON) {
+      const double scale = 1.0 / d.rate_rps;
+      double acc = 0.0;
+      for (int i = 0; i < nr; i++) {
+        acc = acc + scale * np_std_exponential(s.g);  // np.cumsum(exponential(scale, n))
+        arrival[o + i] = (int64_t)rint(acc * 1e9);
+      }
+    } else if (d.arrival_kind == FS_ARRIVAL_FIXED) {
+      for (int i = 0; i < nr; i++) arrival[o + i] = (int64_t)i * d.gap_ns;
+    } else if (d.arrival_kind == FS_ARRIVAL_AT_ZERO) {
+      for (int i = 0; i < nr; i++) arrival[o + i] = 0;
+    } else {
+      atomicExch(&status[k], FS_ERR_VALUE);
+    }
+    return;
+  }
+  const fs_length_dist L = which == 1 ? d.prompt : d.output;
+  int32_t* dst = (which == 1 ? prompt : output) + o;
+  for (int i = 0; i < nr; i++) {
+    int64_t v;
+    if (L.kind == FS_LEN_FIXED) {
+      v = L.value;
+    } else if (L.kind == FS_LEN_UNIFORM) {
+      v = np_integer_dev(s, L.lo, L.hi);
+    } else if (L.kind == FS_LEN_LOGNORMAL) {
+      // random_lognormal = exp(random_normal(mu, sigma)); CUDA's exp (<= 1 ulp) vs
+      // glibc's can only matter when the draw sits on a .5 rounding boundary
+      double x = rint(exp(L.mu + L.sigma * np_std_normal(s.g)));
+      x = x < (double)L.lo ? (double)L.lo : x;
+      x = x > (double)L.hi ? (double)L.hi : x;
+      v = (int64_t)x;
+    } else {
+      atomicExch(&status[k], FS_ERR_VALUE);
+      return;
+    }
+    dst[i] = (int32_t)v;
+  }
+}
+
+// rank of "r{i}" among "r0" .. "r{n-1}" in Python str order, counted per digit
+// length in O(digits^2) (no sort)
+__device__ int32_t id_str_rank_dev(int64_t i, int64_t n) {
+  int dig[20];
+  int m = 0;
+  {
+    int64_t v = i;
+    int tmp[20];
+    do { tmp[m++] = (int)(v % 10); v /= 10; } while (v);
+    for (int q = 0; q < m; q++) dig[q] = tmp[m - 1 - q];
+  }
+  int64_t rank = 0, lo = 0, hi = 10;
+  for (int d = 1; d <= 19 && lo < n; d++) {
+    const int64_t end = hi < n ? hi : n;
+    if (d <= m) {
+      int64_t pre = 0;
+      for (int q = 0; q < d; q++) pre = pre * 10 + dig[q];
+      int64_t c = pre - lo;
+      c = c < 0 ? 0 : (c > end - lo ? end - lo : c);
+      rank += c;
+      if (d < m && pre >= lo && pre < end) rank += 1;  // a proper prefix sorts first
+    } else {
+      int64_t tv = 0, scale = 1;
+      for (int q = 0; q < m; q++) tv = tv * 10 + dig[q];
+      for (int q = 0; q < d - m; q++) scale *= 10;
+      int64_t c = tv * scale - lo;
+      c = c < 0 ? 0 : (c > end - lo ? end - lo : c);
+      rank += c;
+    }
+    lo = hi;
+    hi = hi > INT64_MAX / 10 ? INT64_MAX : hi * 10;
+  }
+  return (int32_t)rank;
+}
+
+__global__ void id_rank_kernel(const fs_workload_desc* __restrict__ w, int n,
+                               int32_t* __restrict__ rank) {
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const int64_t o = w[k].out_offset;
+    const int nr = w[k].n_requests;
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) rank[o + i] = id_str_rank_dev(i, nr);
+  }
+}
+
+int launch_workload(const fs_workload_desc* w, int n, int64_t* arrival, int32_t* prompt,
+                    int32_t* output, int32_t* rank, int32_t* status, void* stream) {
+  if (n <= 0) return 0;
+  const int threads = 128;
+  workload_kernel<<<(3 * n + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
+      w, n, arrival, prompt, output, status);
+  id_rank_kernel<<<n < 148 * 8 ? n : 148 * 8, 64, 0, (cudaStream_t)stream>>>(w, n, rank);
+  return 2;
+}
+
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,
                           const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out,
                           int32_t* status, int n_sms, void* stream) {

@@ -125,6 +125,8 @@ int launch_route_tokens(const int64_t* tokens, const uint64_t* seeds, int n, int
                         int policy, double alpha, double* scratch, int32_t* counts,
                         int32_t* status, void* stream);
 int route_scratch_warps(int n);  // warps (scratch slots) launch_route_tokens uses for n calls
+int launch_workload(const fs_workload_desc* w, int n, int64_t* arrival, int32_t* prompt,
+                    int32_t* output, int32_t* rank, int32_t* status, void* stream);
 int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int32_t* pidx,
                         const int32_t* mb, const int64_t* steps, const int32_t* layers, int n,
                         uint32_t* out, void* stream);

@@ -59,6 +59,7 @@ def load_library(path: str = LIB_PATH):
         "fs_route_uniform": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
         "fs_route_tokens": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, i32, ctypes.c_double, vp,
                                            vp]),
+        "fs_generate_workload": (ctypes.c_int, [vp, vp, i32, vp, vp, vp, vp, vp]),
         "fs_router_seeds": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i32, vp]),
         "fs_set_forests": (ctypes.c_int, [vp, abi.ForestSetC]),
         "fs_attention_forest": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i64, _AttnParamsC, vp]),
@@ -357,6 +358,22 @@ class Engine:
                                              num_experts, top_k, abi.ROUTING[policy], alpha,
                                              abi.ptr(counts), abi.ptr(st)), "fs_route_tokens")
         return counts[:n], st[:n]
+
+    def generate_workload(self, descs):
+        """generate(spec) for fs_workload_desc rows on the device (workload.py:193-216):
+        (arrival_ns int64, prompt int32, output int32, id_rank int32, status per row)."""
+        descs = np.ascontiguousarray(descs, dtype=abi.WORKLOAD_DESC)
+        n = len(descs)
+        total = int((descs["out_offset"] + descs["n_requests"]).max()) if n else 0
+        arr = np.zeros(max(total, 1), np.int64)
+        pr = np.zeros(max(total, 1), np.int32)
+        out = np.zeros(max(total, 1), np.int32)
+        rk = np.zeros(max(total, 1), np.int32)
+        st = np.zeros(max(n, 1), np.int32)
+        self._check(self.lib.fs_generate_workload(self.h, abi.ptr(descs), n, abi.ptr(arr),
+                                                  abi.ptr(pr), abi.ptr(out), abi.ptr(rk),
+                                                  abi.ptr(st)), "fs_generate_workload")
+        return arr[:total], pr[:total], out[:total], rk[:total], st[:n]
 
     def router_seeds(self, prefixes: list[str], prefix_idx, micro_batch, steps, layers):
         from .lower import _prefix
