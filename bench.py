@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 attention-cost kernel leg")
+    ap.add_argument("--no-api", action="store_true", help="skip the simulate() end-to-end leg")
     ap.add_argument("--cpu-sample-seeds", type=int, default=8)
     return ap.parse_args()
 
@@ -365,6 +366,22 @@ def main():
            + raw.done_rank.nbytes)
     assert (raw.rows["iterations"] == res.rows["iterations"]).all()
 
+    # the user-facing call: simulate(config documents) -- parse, validate, draw the
+    # workloads on the device, lower, run, compute_metrics -- timed once per rank
+    api = None
+    if not args.no_api:
+        from paper_2508_03148_b200.api import simulate
+        import copy as _copy
+        simulate(_copy.deepcopy(docs[:64]), engine=eng, device_workload=True)  # warm
+        t0 = time.perf_counter()
+        bundles = simulate(_copy.deepcopy(docs), engine=eng, device_workload=True)
+        api_s = time.perf_counter() - t0
+        n_fail = sum(1 for b in bundles if not hasattr(b, "to_dict"))
+        api = {"value": iters_per_step / api_s, "unit": UNIT, "seconds": api_s,
+               "failures": n_fail,
+               "note": "simulate(docs, device_workload=True): config parsing and validation, "
+                       "device workload generation, lowering, fs_run_batch, compute_metrics"}
+
     # the only collective: gather every rank's fixed-size metric rows (NCCL)
     gather_ms = None
     if world > 1:
@@ -433,6 +450,7 @@ def main():
                          "kernel": "sim_kernel (+metrics_kernel)",
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
             "issue": issue,
+            "api_end_to_end": api,
             "routing": {"draws_per_step": draws_per_step * world,
                         "draws_per_s": draws_per_step * world / (max_ms / args.steps / 1e3),
                         "note": "uniform-router Philox4x64-10 keys (T x E per call) drawn "
