@@ -287,9 +287,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # one rank per GPU; FS_BENCH_BACKEND=gloo runs several ranks on fewer GPUs
+    # (a functional check of the multi-rank path on a 1-GPU box, not a measurement)
+    backend = os.environ.get("FS_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    cdev = f"cuda:{local}" if backend == "nccl" else "cpu"  # device of the collectives' tensors
     from paper_2508_03148_b200 import abi
     from paper_2508_03148_b200.engine import Engine
 
@@ -332,8 +340,8 @@ def main():
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-    its = torch.tensor([iters_per_step * args.steps], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
+    its = torch.tensor([iters_per_step * args.steps], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(its, op=dist.ReduceOp.SUM)
@@ -356,7 +364,7 @@ def main():
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_times.append(dt)
-    e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=f"cuda:{local}")
+    e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = total_its / float(e2e_s.item())
@@ -385,13 +393,18 @@ def main():
     # the only collective: gather every rank's fixed-size metric rows (NCCL)
     gather_ms = None
     if world > 1:
-        rows_t = torch.from_numpy(raw.rows.view(np.uint8).copy()).to(f"cuda:{local}")
+        rows_t = torch.from_numpy(raw.rows.view(np.uint8).copy()).to(cdev)
         out = [torch.empty_like(rows_t) for _ in range(world)]
         torch.cuda.synchronize()
         g0 = time.perf_counter()
         dist.all_gather(out, rows_t)
         torch.cuda.synchronize()
         gather_ms = (time.perf_counter() - g0) * 1e3
+        # every rank's rows arrived intact: their iterations add up to the job total
+        got = sum(int(np.frombuffer(o.cpu().numpy().tobytes(), dtype=abi.METRIC_ROW)
+                      ["iterations"].sum()) for o in out)
+        if got * args.steps != int(total_its):
+            raise SystemExit(f"gathered rows hold {got} iterations, expected {total_its / args.steps}")
 
     # roofline of the dominant kernel (the DES step kernel)
     alg_bytes = algorithmic_bytes(low, res.rows)

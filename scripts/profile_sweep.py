@@ -40,6 +40,8 @@ def main():
     clk = 1.965e9
     for f in "ABC":
         m = fam == f
+        if not m.any():
+            continue
         print(f"family {f}: n={m.sum()} iters={its[m].sum()} cycles mean={cyc[m].mean():.3e} "
               f"max={cyc[m].max():.3e} ({cyc[m].max()/clk*1e3:.1f} ms) "
               f"sum={cyc[m].sum():.3e} cyc/iter={cyc[m].sum()/its[m].sum():.0f}")

@@ -165,3 +165,10 @@ def test_sweep_driver_end_to_end(engine, tmp_path):
         else:
             assert r["status"].startswith("failed: RequestCannotFit")
     assert (tmp_path / "frontier.json").exists()
+
+
+def test_event_budget_boundary_device(engine, golden_scenarios):
+    """core.py:186-191 on the device: exactly enough events passes, one short fails."""
+    from test_oracle_golden import BUDGET_CASES, _budget_specs
+    raw = engine.run(lower(_budget_specs(golden_scenarios, BUDGET_CASES)))
+    assert raw.rows["status"].tolist() == [0, 3] * len(BUDGET_CASES)

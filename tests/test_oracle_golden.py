@@ -82,3 +82,26 @@ def test_python_sum_emulation(golden_pure):
     for xs, want in golden_pure["py_sum"]:
         got = oracle.pysum(xs)
         assert got == want or (math.isnan(got) and math.isnan(want))
+
+
+def _budget_specs(golden_scenarios, names):
+    import dataclasses
+    from parity import specs_for
+    specs = []
+    for n in names:
+        g = golden_scenarios[n]
+        (sp,) = specs_for([g["config"]])
+        specs.append(dataclasses.replace(sp, max_events=g["events"]))      # exactly enough
+        specs.append(dataclasses.replace(sp, max_events=g["events"] - 1))  # one short
+    return specs
+
+
+BUDGET_CASES = ("co_llama_40", "pd_2_3_paged_tight", "af_tiny_moe_m3_dp2", "co_moe_mixtral_ep2")
+
+
+def test_event_budget_boundary_oracle(golden_scenarios):
+    """core.py:186-191: EventBudgetExceeded once processed > max_events."""
+    from oracle import oracle
+    from paper_2508_03148_b200.lower import lower
+    raw = oracle.run(lower(_budget_specs(golden_scenarios, BUDGET_CASES)))
+    assert raw.rows["status"].tolist() == [0, 3] * len(BUDGET_CASES)
