@@ -172,3 +172,26 @@ def test_event_budget_boundary_device(engine, golden_scenarios):
     from test_oracle_golden import BUDGET_CASES, _budget_specs
     raw = engine.run(lower(_budget_specs(golden_scenarios, BUDGET_CASES)))
     assert raw.rows["status"].tolist() == [0, 3] * len(BUDGET_CASES)
+
+
+def test_baseline_full_sizes_vs_oracle_with_invariants(engine):
+    """BASELINE C1 (1,000 requests) and C4 (AF m=2 and EP=8, DeepSeek-V3 shape) at the
+    GPU's 64-request instance size: device == oracle on every output, plus
+    size-independent properties -- every request completes after its first token,
+    every router call tallies exactly T * top_k expert slots, iterations add up."""
+    from oracle import oracle
+    from parity import run_backend
+    docs = [W.c1_colocated(1000, seed=7), W.c4_af(64, seed=5), W.c4_colocated_ep(64, seed=6)]
+    low = lower([instance_spec(parse_config(copy.deepcopy(d))) for d in docs])
+    dev = engine.run(low)
+    assert (dev.rows["status"] == 0).all()
+    assert_same_raw(dev, oracle.run(low, threads=3))
+    res = run_backend(engine, docs, routes=True)
+    for r, d in zip(res, docs):
+        assert r.ok
+        assert (r.first_token_ns >= r.arrival_ns).all() and (r.done_ns >= r.first_token_ns).all()
+        assert sorted(r.completion_order()) == sorted(r.request_ids)
+        k = d["model"].get("moe", {}).get("top_k", 0)
+        for rt in (r.routes or []):
+            assert sum(rt["counts"]) == rt["tokens"] * k
+        assert r.iterations == len(r.batches)
