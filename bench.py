@@ -50,6 +50,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the C2 attention-cost kernel leg")
     ap.add_argument("--no-api", action="store_true", help="skip the simulate() end-to-end leg")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config (C1/C3/C4) batches")
     ap.add_argument("--cpu-sample-seeds", type=int, default=8)
     return ap.parse_args()
 
@@ -275,6 +277,53 @@ def bench_attention_cost(eng, device: int, steps: int, warmup: int, n_batches: i
     return res
 
 
+def bench_configs(device: int, reps: int = 2):
+    """The other BASELINE.json configs as batches of independent seeds on one GPU:
+    C1 (Llama-2-7B co-located, 1,000 requests), C3 (PD 70B, tight 30 GB decode
+    pool), C4 (DeepSeek-V3 AF m=2 and co-located EP=8, 64 requests). Each row:
+    instances, iterations, device ms per batch (CUDA events, inputs resident)
+    and the C port of the reference on one host core for one instance."""
+    import torch
+
+    from oracle import oracle
+    from paper_2508_03148_b200 import workloads as W
+    from paper_2508_03148_b200.engine import Engine
+    cases = {
+        "C1_colocated_llama7b_1000req": (lambda s: W.c1_colocated(1000, seed=s), 296),
+        "C3_pd_70b_tight_300req": (lambda s: W.c3_pd(300, seed=s, tight=True), 296),
+        "C4_af_dsv3_m2_64req": (lambda s: W.c4_af(64, seed=s), 148),
+        "C4_colocated_dsv3_ep8_64req": (lambda s: W.c4_colocated_ep(64, seed=s), 148),
+    }
+    out = {}
+    stream = torch.cuda.Stream(device=device)
+    for name, (make, n) in cases.items():
+        low = lower_docs([make(1 + i) for i in range(n)])
+        eng = Engine(device)
+        eng.stage(low)
+        eng.launch(stream.cuda_stream)
+        torch.cuda.synchronize()
+        rows = eng.fetch(low, per_request=False).rows
+        ms = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            eng.launch(stream.cuda_stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        its = int(rows["iterations"].sum())
+        one = lower_docs([make(1)])
+        t0 = time.perf_counter()
+        ref = oracle.run(one, threads=1)
+        cpu_s = time.perf_counter() - t0
+        out[name] = {"instances": n, "iterations": its, "ms": min(ms),
+                     "iterations_per_s": its / (min(ms) / 1e3),
+                     "all_ok": bool((rows["status"] == 0).all()),
+                     "routing_draws": int(rows["routing_draws"].sum()),
+                     "cpu_port_1core_iterations_per_s": int(ref.rows["iterations"][0]) / cpu_s}
+    return out
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
@@ -432,6 +481,10 @@ def main():
     if not args.no_c2:
         c2 = bench_attention_cost(eng, local, args.steps, args.warmup)
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = bench_configs(local)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_count()
@@ -474,6 +527,7 @@ def main():
             "gather_ms": gather_ms,
             "step_ms": step_ms,
             "c2_attention_cost": c2,
+            "baseline_configs": configs,
         }
         print(json.dumps(line))
     if world > 1:
