@@ -271,11 +271,12 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
     // dirichlet_skew routing is compiled into the extended (learned) kernel variant only
     if (descs[i].has_moe && descs[i].routing_policy == FS_ROUTE_DIRICHLET) e->learned = true;
   }
-  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned, e->sim_ctas);
-  P.chunk_blocks = e->chunk_blocks;
   int max_e = 0;
   for (int i = 0; i < n_instances; i++)
     if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);
+  // MoE batches launch the full wave: warps without an instance help route
+  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned, e->sim_ctas, max_e > 0);
+  P.chunk_blocks = e->chunk_blocks;
   P.job_max_e = std::min(max_e, FS_MAX_EXPERTS);
   FS_CHECK(e->inst_done.ensure(2 * sizeof(int32_t)));
   P.inst_done = e->inst_done.as<int32_t>();

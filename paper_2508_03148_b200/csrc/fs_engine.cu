@@ -22,9 +22,9 @@ void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void*
   midstate_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(prefixes, mid, n);
 }
 
-int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm) {
-  return learned ? learned::slots(n_sms, n_inst, ctas_per_sm)
-                 : analytic::slots(n_sms, n_inst, ctas_per_sm);
+int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm, bool helpers) {
+  return learned ? learned::slots(n_sms, n_inst, ctas_per_sm, helpers)
+                 : analytic::slots(n_sms, n_inst, ctas_per_sm, helpers);
 }
 
 int launch_simulation(const EngineParams& p, bool learned, void* stream) {

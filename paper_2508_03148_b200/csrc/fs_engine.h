@@ -101,15 +101,15 @@ struct EngineParams {
 void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void* stream);
 // simulation kernel variants (fs_sim.cuh compiled twice)
 namespace analytic {
-int slots(int n_sms, int n_inst, int ctas_per_sm);
+int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
 int launch(const EngineParams& p, void* stream);
 }  // namespace analytic
 namespace learned {
-int slots(int n_sms, int n_inst, int ctas_per_sm);
+int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
 int launch(const EngineParams& p, void* stream);
 }  // namespace learned
 // ctas_per_sm <= 0: as many simulation CTAs per SM as fit
-int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm);
+int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm, bool helpers);
 int launch_simulation(const EngineParams& p, bool learned, void* stream);
 int launch_metrics(const EngineParams& p, void* stream);
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,

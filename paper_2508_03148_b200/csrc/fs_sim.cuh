@@ -1877,7 +1877,11 @@ static size_t sim_dyn_smem() {
   return bytes;
 }
 
-int slots(int n_sms, int n_inst, int ctas_per_sm) {
+// Grid: one resident wave. Without routing jobs a batch smaller than the wave
+// gets one warp per instance; with them (MoE instances) the whole wave runs, so
+// the warps beyond the instance count start as job-board helpers -- a batch of
+// 148 DeepSeek-V3 instances otherwise has one warp per SM for 39 G router keys.
+int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sim_kernel, 32 * kWarpsPerCta,
                                                 sim_dyn_smem());
@@ -1885,7 +1889,7 @@ int slots(int n_sms, int n_inst, int ctas_per_sm) {
   if (per_sm < 1) per_sm = 1;
   const int need = (n_inst + kWarpsPerCta - 1) / kWarpsPerCta;
   int grid = n_sms * per_sm;
-  if (grid > need) grid = need;
+  if (grid > need && !helpers) grid = need;
   if (grid < 1) grid = 1;
   return grid * kWarpsPerCta;
 }
