@@ -49,6 +49,9 @@
 #ifndef FS_DIR_IN_ANALYTIC
 #define FS_DIR_IN_ANALYTIC 0
 #endif
+#ifndef FS_LONG_ROW_UNROLL  // unrolled Philox rounds for long row segments (>= 64 draws):
+#define FS_LONG_ROW_UNROLL 0  // C4 EP 430 -> 373 ms, but the C5 sweep 272 -> ~300 ms (code size)
+#endif
 
 namespace fs {
 namespace FS_SIM_NS {
@@ -418,7 +421,13 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
     if (b + 1 <= blast) consume(B, b + 1);
   }
 #else
-  for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) consume(philox4x64_10(b + 1, k0, k1), b);
+  if (FS_LONG_ROW_UNROLL && n1 - n0 >= 64) {
+    // long rows (E >= 64 per segment): the unrolled rounds, see philox4x64_10_unrolled
+    for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++)
+      consume(philox4x64_10_unrolled(b + 1, k0, k1), b);
+  } else {
+    for (uint64_t b = n0 >> 2; b <= (n1 - 1) >> 2; b++) consume(philox4x64_10(b + 1, k0, k1), b);
+  }
 #endif
 }
 
