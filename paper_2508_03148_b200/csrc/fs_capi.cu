@@ -61,6 +61,7 @@ struct fs_engine {
   DevBuf f_descs, f_roots, f_right, f_value, f_leaf;  // f_value: packed NodeP array
   fs::ForestView fv{};
   bool learned = false;  // staged batch uses the learned simulation variant
+  int variant = 0;       // fs::SimVariant of the staged batch
   // routing job geometry (environment knobs read at fs_create)
   int sim_ctas = 0;          // FS_SIM_CTAS_PER_SM (0 = as many as fit)
   int chunk_blocks = 96;     // FS_CHUNK_BLOCKS: Philox blocks per lane per job chunk
@@ -274,8 +275,13 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   int max_e = 0;
   for (int i = 0; i < n_instances; i++)
     if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);
+  // kernel variant: learned models / dirichlet need the extended kernel; long MoE
+  // rows (>= 64 experts) the long-row one; everything else the sweep kernel
+  e->variant = e->learned ? fs::kSimLearned
+                          : (max_e >= 64 && !getenv("FS_NO_LONGROW") ? fs::kSimLongRow
+                                                                      : fs::kSimAnalytic);
   // MoE batches launch the full wave: warps without an instance help route
-  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->learned, e->sim_ctas, max_e > 0);
+  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->variant, e->sim_ctas, max_e > 0);
   P.chunk_blocks = e->chunk_blocks;
   P.job_max_e = std::min(max_e, FS_MAX_EXPERTS);
   FS_CHECK(e->inst_done.ensure(2 * sizeof(int32_t)));
@@ -320,7 +326,7 @@ int fs_launch_async(fs_engine* e, void* stream) {
   if (e->params.jobs)
     FS_CHECK(cudaMemsetAsync(e->jobs.p, 0, (size_t)e->params.n_slots * sizeof(fs::RouteJob), s));
   e->last_launches = 0;
-  e->last_launches += fs::launch_simulation(e->params, e->learned, s);
+  e->last_launches += fs::launch_simulation(e->params, e->variant, s);
   e->last_launches += fs::launch_metrics(e->params, s);
   FS_CHECK(cudaGetLastError());
   return 0;

@@ -22,13 +22,16 @@ void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void*
   midstate_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(prefixes, mid, n);
 }
 
-int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm, bool helpers) {
-  return learned ? learned::slots(n_sms, n_inst, ctas_per_sm, helpers)
-                 : analytic::slots(n_sms, n_inst, ctas_per_sm, helpers);
+int simulation_slots(int n_sms, int n_inst, int variant, int ctas_per_sm, bool helpers) {
+  if (variant == kSimLearned) return learned::slots(n_sms, n_inst, ctas_per_sm, helpers);
+  if (variant == kSimLongRow) return longrow::slots(n_sms, n_inst, ctas_per_sm, helpers);
+  return analytic::slots(n_sms, n_inst, ctas_per_sm, helpers);
 }
 
-int launch_simulation(const EngineParams& p, bool learned, void* stream) {
-  return learned ? learned::launch(p, stream) : analytic::launch(p, stream);
+int launch_simulation(const EngineParams& p, int variant, void* stream) {
+  if (variant == kSimLearned) return learned::launch(p, stream);
+  if (variant == kSimLongRow) return longrow::launch(p, stream);
+  return analytic::launch(p, stream);
 }
 
 }  // namespace fs

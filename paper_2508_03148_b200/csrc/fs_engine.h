@@ -108,9 +108,16 @@ namespace learned {
 int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
 int launch(const EngineParams& p, void* stream);
 }  // namespace learned
+namespace longrow {
+int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
+int launch(const EngineParams& p, void* stream);
+}  // namespace longrow
+// simulation kernel variants: analytic (the sweep kernel), learned (learned models,
+// dirichlet routing), longrow (analytic, MoE rows of >= 64 experts)
+enum SimVariant { kSimAnalytic = 0, kSimLearned = 1, kSimLongRow = 2 };
 // ctas_per_sm <= 0: as many simulation CTAs per SM as fit
-int simulation_slots(int n_sms, int n_inst, bool learned, int ctas_per_sm, bool helpers);
-int launch_simulation(const EngineParams& p, bool learned, void* stream);
+int simulation_slots(int n_sms, int n_inst, int variant, int ctas_per_sm, bool helpers);
+int launch_simulation(const EngineParams& p, int variant, void* stream);
 int launch_metrics(const EngineParams& p, void* stream);
 int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* off,
                           const uint8_t* dec, int64_t nb, fs_attn_params prm, double* out,
