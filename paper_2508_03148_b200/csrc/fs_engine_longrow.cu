@@ -5,4 +5,5 @@
 #define FS_LEARNED 0
 #define FS_SIM_NS longrow
 #define FS_LONG_ROW_UNROLL 1
+#define FS_TOPK_BRANCHFREE 1
 #include "fs_sim.cuh"

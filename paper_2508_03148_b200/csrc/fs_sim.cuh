@@ -49,6 +49,9 @@
 #ifndef FS_DIR_IN_ANALYTIC
 #define FS_DIR_IN_ANALYTIC 0
 #endif
+#ifndef FS_TOPK_BRANCHFREE  // insert every key (no threshold test): in a warp some lane
+#define FS_TOPK_BRANCHFREE 0  // almost always inserts, so the test only adds instructions
+#endif
 #ifndef FS_LONG_ROW_UNROLL  // unrolled Philox rounds for long row segments (>= 64 draws):
 #define FS_LONG_ROW_UNROLL 0  // C4 EP 430 -> 373 ms, but the C5 sweep 272 -> ~300 ms (code size)
 #endif
@@ -395,14 +398,14 @@ __device__ __forceinline__ void pass_fast(uint32_t (&top)[KCAP], int kc, bool ac
     for (int j = 0; j < 4; j++) {
       if (j >= jlo && j < jhi) {
         uint32_t x = ((uint32_t)(blk.v[j] >> 32) & ~emask) | (eb0 + (uint32_t)j);
-        if (KCAP <= 4 || x < thr) {
+        if (KCAP <= 4 || FS_TOPK_BRANCHFREE || x < thr) {
 #pragma unroll
           for (int q = 0; q < KCAP; q++) {
             const uint32_t lo = min(top[q], x);
             x = max(top[q], x);
             top[q] = lo;
           }
-          if (KCAP > 4) {
+          if (KCAP > 4 && !FS_TOPK_BRANCHFREE) {
 #pragma unroll
             for (int q = 0; q < KCAP; q++)
               if (q == kc - 1) thr = top[q];
