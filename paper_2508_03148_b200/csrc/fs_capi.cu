@@ -62,6 +62,8 @@ struct fs_engine {
   fs::ForestView fv{};
   bool learned = false;  // staged batch uses the learned simulation variant
   int variant = 0;       // fs::SimVariant of the staged batch
+  int n_moe = 0;         // MoE instances of the staged batch (first in the order)
+  int split_families = 1;  // FS_SPLIT_FAMILIES: MoE and dense instances in separate waves
   // routing job geometry (environment knobs read at fs_create)
   int sim_ctas = 0;          // FS_SIM_CTAS_PER_SM (0 = as many as fit)
   int chunk_blocks = 96;     // FS_CHUNK_BLOCKS: Philox blocks per lane per job chunk
@@ -121,6 +123,7 @@ int fs_create(int device, fs_engine** out) {
     return v && *v ? atoi(v) : dflt;
   };
   e->sim_ctas = env_int("FS_SIM_CTAS_PER_SM", 0);
+  e->split_families = env_int("FS_SPLIT_FAMILIES", 1);
   e->chunk_blocks = env_int("FS_CHUNK_BLOCKS", 96);
   if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete e;
@@ -191,8 +194,14 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   // longest estimated cost first (the work queue is consumed in this order)
   std::vector<int32_t> order(n_instances);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return descs[a].est_cost > descs[b].est_cost; });
+  // MoE instances first, then the dense ones; each group longest estimated cost
+  // first. fs_launch_async runs the two groups as separate waves (see there).
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    if (descs[a].has_moe != descs[b].has_moe) return descs[a].has_moe > descs[b].has_moe;
+    return descs[a].est_cost > descs[b].est_cost;
+  });
+  e->n_moe = 0;
+  for (int i = 0; i < n_instances; i++) e->n_moe += descs[i].has_moe ? 1 : 0;
 
   FS_CHECK(upload(e->descs, descs, n_instances, s));
   FS_CHECK(upload(e->reps, replicas, n_replicas, s));
@@ -326,7 +335,22 @@ int fs_launch_async(fs_engine* e, void* stream) {
   if (e->params.jobs)
     FS_CHECK(cudaMemsetAsync(e->jobs.p, 0, (size_t)e->params.n_slots * sizeof(fs::RouteJob), s));
   e->last_launches = 0;
-  e->last_launches += fs::launch_simulation(e->params, e->variant, s);
+  const int n = e->params.n_inst, nm = e->n_moe;
+  if (e->split_families && nm > 0 && nm < n) {
+    // Two waves: the MoE instances (routing-heavy code) then the dense ones. Mixed
+    // on the same SMs the two code paths fight over instruction fetch: the C5 sweep
+    // takes 280 ms mixed, 184 + 71 ms as separate waves.
+    fs::EngineParams moe = e->params, dense = e->params;
+    moe.n_inst = nm;
+    dense.n_inst = n - nm;
+    dense.order = e->params.order + nm;
+    e->last_launches += fs::launch_simulation(moe, e->variant, s);
+    FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
+    FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
+    e->last_launches += fs::launch_simulation(dense, e->variant, s);
+  } else {
+    e->last_launches += fs::launch_simulation(e->params, e->variant, s);
+  }
   e->last_launches += fs::launch_metrics(e->params, s);
   FS_CHECK(cudaGetLastError());
   return 0;

@@ -68,7 +68,8 @@ def test_c_client_matches_python_binding(engine, tmp_path):
     req = np.fromfile(tmp_path / "req.bin", dtype=np.int64).reshape(2, -1)
     assert rows.tobytes() == ref.rows.tobytes()
     assert np.array_equal(req[0], ref.first_ns) and np.array_equal(req[1], ref.done_ns)
-    assert lines[0].startswith("run_batch") and "launches=2" in lines[0]
+    assert lines[0].startswith("run_batch")
+    assert f"launches={engine.last_launch_count}" in lines[0]  # same kernels as the binding
 
     spec = WorkloadSpec(ArrivalSpec("poisson", rate_rps=20.0),
                         LengthDist("lognormal", lo=8, hi=4096, mu=6.0, sigma=1.0),
