@@ -64,6 +64,7 @@ struct fs_engine {
   int variant = 0;       // fs::SimVariant of the staged batch
   int n_moe = 0;         // MoE instances of the staged batch (first in the order)
   int split_families = 1;  // FS_SPLIT_FAMILIES: MoE and dense instances in separate waves
+  int dense_variant = 1;   // FS_DENSE_VARIANT: dense instances on the MoE-free kernel
   // routing job geometry (environment knobs read at fs_create)
   int sim_ctas = 0;          // FS_SIM_CTAS_PER_SM (0 = as many as fit)
   int chunk_blocks = 96;     // FS_CHUNK_BLOCKS: Philox blocks per lane per job chunk
@@ -124,6 +125,7 @@ int fs_create(int device, fs_engine** out) {
   };
   e->sim_ctas = env_int("FS_SIM_CTAS_PER_SM", 0);
   e->split_families = env_int("FS_SPLIT_FAMILIES", 1);
+  e->dense_variant = env_int("FS_DENSE_VARIANT", 1);
   e->chunk_blocks = env_int("FS_CHUNK_BLOCKS", 96);
   if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete e;
@@ -289,6 +291,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   e->variant = e->learned ? fs::kSimLearned
                           : (max_e >= 64 && !getenv("FS_NO_LONGROW") ? fs::kSimLongRow
                                                                       : fs::kSimAnalytic);
+  if (e->variant == fs::kSimAnalytic && max_e == 0 && e->dense_variant) e->variant = fs::kSimDense;
   // MoE batches launch the full wave: warps without an instance help route
   P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->variant, e->sim_ctas, max_e > 0);
   P.chunk_blocks = e->chunk_blocks;
@@ -347,7 +350,8 @@ int fs_launch_async(fs_engine* e, void* stream) {
     e->last_launches += fs::launch_simulation(moe, e->variant, s);
     FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
     FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
-    e->last_launches += fs::launch_simulation(dense, e->variant, s);
+    const int dv = (e->variant != fs::kSimLearned && e->dense_variant) ? fs::kSimDense : e->variant;
+    e->last_launches += fs::launch_simulation(dense, dv, s);
   } else {
     e->last_launches += fs::launch_simulation(e->params, e->variant, s);
   }

@@ -25,12 +25,14 @@ void launch_midstate(const fs_seed_prefix* prefixes, uint32_t* mid, int n, void*
 int simulation_slots(int n_sms, int n_inst, int variant, int ctas_per_sm, bool helpers) {
   if (variant == kSimLearned) return learned::slots(n_sms, n_inst, ctas_per_sm, helpers);
   if (variant == kSimLongRow) return longrow::slots(n_sms, n_inst, ctas_per_sm, helpers);
+  if (variant == kSimDense) return dense::slots(n_sms, n_inst, ctas_per_sm, helpers);
   return analytic::slots(n_sms, n_inst, ctas_per_sm, helpers);
 }
 
 int launch_simulation(const EngineParams& p, int variant, void* stream) {
   if (variant == kSimLearned) return learned::launch(p, stream);
   if (variant == kSimLongRow) return longrow::launch(p, stream);
+  if (variant == kSimDense) return dense::launch(p, stream);
   return analytic::launch(p, stream);
 }
 

@@ -49,6 +49,9 @@
 #ifndef FS_DIR_IN_ANALYTIC
 #define FS_DIR_IN_ANALYTIC 0
 #endif
+#ifndef FS_DENSE_ONLY  // the MoE paths compiled out (the dense wave's kernel variant)
+#define FS_DENSE_ONLY 0
+#endif
 #ifndef FS_TOPK_BRANCHFREE  // insert every key (no threshold test): in a warp some lane
 #define FS_TOPK_BRANCHFREE 0  // almost always inserts, so the test only adds instructions
 #endif
@@ -907,7 +910,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
   const double coll = tpcoll_us(d, c, n);
   PySum ls;
   ls.init();
-  if (!d->has_moe) {
+  if (FS_DENSE_ONLY || !d->has_moe) {
     const double ffn = FFN_DENSE_US(c, n);
     double tot = qkv + att;
     tot = tot + out;
@@ -1586,7 +1589,7 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
       sm->af_size[i] = sz;
     }
     // FFN durations per layer (af.py:289-301): MoE routes with the uniform policy
-    if (!d->has_moe) {
+    if (FS_DENSE_ONLY || !d->has_moe) {
       double f = FFN_DENSE_US(cf, sz);
       f = f + tpcoll_us(d, cf, sz);
       const int64_t fns = py_round(f * 1000.0);
@@ -1768,6 +1771,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
   I.log_batches = I.log_moff = I.log_eoff = I.log_routes = 0;
 
   if (I.R > FS_MAX_REPLICAS || (d->has_moe && d->num_experts > FS_MAX_EXPERTS)) fail(I, FS_ERR_CAPACITY, 0);
+  if (FS_DENSE_ONLY && d->has_moe) fail(I, FS_ERR_INTERNAL, 9);  // host dispatch error
 #if FS_LEARNED
   {
     const int fsel[2] = {d->attn_forest, d->gg_forest};
@@ -1874,7 +1878,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, FS_SIM_MIN_BLOCKS) sim_kern
     if (k >= P.n_inst) break;
     simulate_instance(P, P.order[k], lane, blockIdx.x * kWarpsPerCta + w, sm, slab);
   }
-  if (P.jobs) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w, sm->counts);
+  if (P.jobs && !FS_DENSE_ONLY) help_route_jobs(P, lane, blockIdx.x * kWarpsPerCta + w, sm->counts);
 }
 
 // Persistent grid: every CTA resident at once (the job board relies on warps
