@@ -183,9 +183,23 @@ def ncu_summary(kernel: str) -> dict:
     return {}
 
 
+def ncu_kernels(kernel: str) -> list[dict]:
+    """Every summary entry of `kernel` (variants: analytic::sim_kernel, dense::sim_kernel)."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+    except Exception:
+        return []
+    return [v for name, v in d.items()
+            if name == kernel or name.startswith(kernel + "_") or name.endswith("::" + kernel)]
+
+
 def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
-    return ncu_summary(kernel).get("dram_bytes_per_launch")
+    """dram bytes per step of `kernel` (all its launches in one step) from the
+    committed ncu --set full summary."""
+    ks = [k.get("dram_bytes_per_launch") for k in ncu_kernels(kernel)]
+    return sum(ks) if ks and None not in ks else None
 
 
 def algorithmic_bytes(low, rows) -> int:
@@ -466,7 +480,10 @@ def main():
     # instruction roofline from the committed ncu capture (warp instructions per
     # launch, same workload) over this run's step time vs 148 SMs x 4 issue/clk
     issue = None
-    summ = ncu_summary("sim_kernel")
+    sims = ncu_kernels("sim_kernel")  # the MoE wave and the dense wave of a step
+    summ = {"warp_instructions": sum(k.get("warp_instructions", 0) for k in sims),
+            "issue_active_pct": [k.get("issue_active_pct") for k in sims],
+            "source": sorted({k.get("source") for k in sims})} if sims else {}
     if summ.get("warp_instructions"):
         sm_mhz = (clocks.summary() or {}).get("sm_max_mhz") or 1965.0
         peak_ips = 148 * 4 * sm_mhz * 1e6
@@ -513,7 +530,7 @@ def main():
                     "d2h_bytes_per_step": int(d2h), "host_lowering_s": t_low},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "sim_kernel (+metrics_kernel)",
+                         "kernel": "sim_kernel: MoE wave (analytic) + dense wave (dense variant)",
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
             "issue": issue,
             "api_end_to_end": api,

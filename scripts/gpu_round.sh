@@ -35,7 +35,7 @@ if [[ $STAGES == *l* ]]; then
   echo "launch list exit $?"
 fi
 if [[ $STAGES == *f* ]]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sim_kernel -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sim_kernel -c 2 \
     -f -o $OUT/sim_full_$TAG python scripts/profile_sweep.py 64 > $OUT/sim_full_$TAG.log 2>&1
   echo "sim full exit $?"
   timeout 600 ncu --set full --clock-control none --import-source on \

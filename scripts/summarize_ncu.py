@@ -30,7 +30,8 @@ def main(rep, out, tag):
     hdr, units, data = rows[0], rows[1], rows[2:]
     res = {}
     for r in data:
-        name = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+        parts = r[hdr.index("Kernel Name")].split("(")[0].split("::")
+        name = "::".join(parts[-2:]) if len(parts) > 2 else parts[-1]  # e.g. dense::sim_kernel
         d = {}
         for k, short in WANT.items():
             if k in hdr:
