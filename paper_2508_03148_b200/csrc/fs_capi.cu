@@ -351,6 +351,9 @@ int fs_launch_async(fs_engine* e, void* stream) {
     FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
     FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
     const int dv = (e->variant != fs::kSimLearned && e->dense_variant) ? fs::kSimDense : e->variant;
+    if (dv == fs::kSimDense)  // its own resident wave (slots only index routing jobs,
+                              // which the dense variant has none of)
+      dense.n_slots = fs::simulation_slots(e->n_sms, n - nm, dv, e->sim_ctas, false);
     e->last_launches += fs::launch_simulation(dense, dv, s);
   } else {
     e->last_launches += fs::launch_simulation(e->params, e->variant, s);

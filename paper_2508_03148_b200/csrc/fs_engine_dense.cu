@@ -4,4 +4,5 @@
 #define FS_LEARNED 0
 #define FS_SIM_NS dense
 #define FS_DENSE_ONLY 1
+#define FS_SIM_MIN_BLOCKS 3  // 176 -> <= 168 registers: three CTAs (12 warps) per SM
 #include "fs_sim.cuh"

@@ -46,7 +46,11 @@ def main(rep, out, tag):
             d["dram_bytes_per_launch"] = d["dram_read"] + d["dram_write"]
         d["units_note"] = "bytes, seconds"
         d["source"] = tag
-        res.setdefault(name, d)
+        base, n = name, 2
+        while name in res:  # a second launch of the same kernel (e.g. the dense wave)
+            name = f"{base}_{n}"
+            n += 1
+        res[name] = d
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1, sort_keys=True)
     print(json.dumps(res, indent=1))
