@@ -195,11 +195,13 @@ def ncu_kernels(kernel: str) -> list[dict]:
             if name == kernel or name.startswith(kernel + "_") or name.endswith("::" + kernel)]
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per step of `kernel` (all its launches in one step) from the
-    committed ncu --set full summary."""
+def ncu_traffic(kernel: str, waves: bool = False):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary;
+    waves=True sums its launches within one step (the sim kernel's two waves)."""
     ks = [k.get("dram_bytes_per_launch") for k in ncu_kernels(kernel)]
-    return sum(ks) if ks and None not in ks else None
+    if not ks or None in ks:
+        return None
+    return sum(ks) if waves else ks[0]
 
 
 def algorithmic_bytes(low, rows) -> int:
@@ -474,7 +476,7 @@ def main():
     peak, peak_kind = measured_peaks()
     avg_ms = max_ms / args.steps
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
-    traffic = ncu_traffic("sim_kernel")
+    traffic = ncu_traffic("sim_kernel", waves=True)
 
     # the DES step kernel is instruction-issue bound, not HBM bound: its
     # instruction roofline from the committed ncu capture (warp instructions per
