@@ -274,9 +274,12 @@ __global__ void __launch_bounds__(256) attention_cost_kernel_tpb(
 // start on a 16-byte boundary), partial sums meet by shuffle, and the group
 // leader runs the fp64 tail. A tile that does not fit a stage (long batches) or
 // whose widened range would read past the arrays runs from global memory.
+#ifndef FS_C2_STAGES  // ring depth: 2 stages = 41 KB per CTA, 5 CTAs (20 warps) per SM
+#define FS_C2_STAGES 2
+#endif
 constexpr int kC2TileBatches = 32;   // 4 warps x 8 batches
 constexpr int kC2Threads = 128;      // 4 threads per batch
-constexpr int kC2Stages = 4;
+constexpr int kC2Stages = FS_C2_STAGES;
 constexpr int kC2StageElems = 2560;  // per array: 32 x 72 members + alignment slack
 
 struct C2Smem {
@@ -356,7 +359,20 @@ __global__ void __launch_bounds__(kC2Threads) attention_cost_kernel_tma(
     const int st = it % kC2Stages;
     c2_wait(S, st, (uint32_t)((it / kC2Stages) & 1));
     const int64_t base = S.base[st];
-    const int64_t b = t * kC2TileBatches + grp;
+    // phase-sorted assignment inside the tile: decode batches to the first
+    // groups, prefill batches to the rest, so a warp's eight batches mostly share
+    // a phase and the decode-only / prefill-only work does not diverge
+    const int64_t tb0 = t * kC2TileBatches;
+    const int ntile = (int)min((int64_t)kC2TileBatches, nb - tb0);
+    const int lane = tid & 31;
+    const bool ldec = lane < ntile && __ldg(dec + tb0 + lane) != 0;
+    const unsigned dmask = __ballot_sync(FS_FULL, ldec);
+    const unsigned valid = ntile >= 32 ? 0xFFFFFFFFu : ((1u << ntile) - 1u);
+    const int nd = __popc(dmask);
+    int pos = ntile;  // groups beyond the tile do nothing
+    if (grp < nd) pos = (int)__fns(dmask, 0, grp + 1);
+    else if (grp < ntile) pos = (int)__fns(~dmask & valid, 0, grp - nd + 1);
+    const int64_t b = pos < ntile ? tb0 + pos : nb;
     int64_t sq = 0, skv = 0, sall = 0, seq = 0, o0 = 0, o1 = 0;
     int bad = 0, ml = 0, mc = 0;
     bool d = false;
@@ -585,8 +601,8 @@ int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* of
                           int32_t* status, int n_sms, void* stream) {
   if (nb <= 0) return 0;
   const int threads = 256;
-  // "tpb" (default: 167 us for 2^20 x 72-request batches), "tma" (313 us: DRAM reads
-  // exactly the algorithmic bytes but 8 warps/SM leave it latency bound), "warp"
+  // "tpb" (default: 166 us for 2^20 x 72-request batches), "tma" (181 us: DRAM reads
+  // exactly the algorithmic bytes, latency bound on the member loop), "warp"
   const char* mode = getenv("FS_C2");
   if (mode != nullptr && strcmp(mode, "tma") == 0) {
     static bool configured = false;
