@@ -195,3 +195,20 @@ def test_baseline_full_sizes_vs_oracle_with_invariants(engine):
         for rt in (r.routes or []):
             assert sum(rt["counts"]) == rt["tokens"] * k
         assert r.iterations == len(r.batches)
+
+
+@pytest.mark.parametrize("env", [{"FS_SPLIT_FAMILIES": "0"}, {"FS_DENSE_VARIANT": "0"},
+                                 {"FS_CHUNK_BLOCKS": "16"}, {"FS_NO_LONGROW": "1"}])
+def test_dispatch_knobs_do_not_change_results(engine, env, monkeypatch):
+    """Wave split, kernel-variant choice and chunk geometry are scheduling only:
+    a mixed batch (dense, Mixtral, DeepSeek-V3, PD) gives the same bytes."""
+    from paper_2508_03148_b200.engine import Engine
+    docs = W.c5_sweep(n_seeds=1)[::3] + [W.c4_colocated_ep(8, seed=3), W.c3_pd(20, seed=4)]
+    low = lower([instance_spec(parse_config(copy.deepcopy(d))) for d in docs])
+    want = engine.run(low)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    other = Engine(0)  # knobs are read when the engine is created
+    got = other.run(low)
+    assert got.rows.tobytes() == want.rows.tobytes()
+    assert np.array_equal(got.first_ns, want.first_ns) and np.array_equal(got.done_ns, want.done_ns)
