@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FS_ABI_VERSION 1
+#define FS_ABI_VERSION 2
 
 /* Limits of the device engine (checked by the host lowering; violations are
  * reported as FS_ERR_CAPACITY rather than silently truncated). */
@@ -82,8 +82,7 @@ enum fs_status {
   FS_ERR_INVALID_TOPK = 8,         /* costmodel/routing.py:21 InvalidTopK                 */
   FS_ERR_ROUTING_TIE = 9,          /* exact key tie at the top-k boundary: argpartition's
                                       choice is implementation-defined; flagged, not guessed */
-  FS_ERR_UNSUPPORTED = 10,         /* feature not on the device path yet (learned grouped
-                                      GEMM on MoE layers)                                  */
+  FS_ERR_UNSUPPORTED = 10,         /* reserved: no current device path returns it          */
   FS_ERR_CAPACITY = 11,            /* engine limit (FS_MAX_*) exceeded                     */
   FS_ERR_INTERNAL = 12,            /* invariant violated inside the engine                 */
   FS_ERR_VALUE = 13,               /* ValueError raised by a cost-model argument check     */
@@ -258,7 +257,48 @@ typedef struct {
   int32_t member_offset;      /* into members[] (instance-relative) */
   int32_t moe_offset;         /* into moe_ratio[] (instance-relative), -1 if none */
   int32_t n_moe;
-} fs_batch_rec;               /* 40 bytes */
+  int64_t seq;                /* sequence number of the BATCH_COMPLETE event (core.py:160) */
+  int64_t pool_used;          /* replica.pool.snapshot()["used_tokens"] when the batch
+                                 started (base.py:239-246; af.py:494-505) */
+  int64_t af_step;            /* AF step id (af.py:477), -1 otherwise */
+} fs_batch_rec;               /* 64 bytes; recorded when the batch starts, so records are
+                                 in start order: sort by (t_complete, seq) for completion
+                                 order */
+
+/* Event-trace record: one per scheduled event, stored at index `seq` of the
+ * instance's event array (every scheduled event is dispatched, so a complete
+ * run fills 0..event_count-1). The trace the reference returns from
+ * ServingSimulation.run() (core.py:85-129) is these records in (t, seq) order,
+ * rendered as `t,seq,KIND,canonical_json(payload)` (paper_2508_03148_b200/trace.py).
+ * Fields by kind (request / replica are instance-local indices):
+ *   REQUEST_ARRIVAL          a = request
+ *   BATCH_START              replica
+ *   BATCH_COMPLETE           replica, a = index of its fs_batch_rec
+ *   PREFILL_COMPLETE         replica, a = request
+ *   MEMORY_AVAILABLE         replica, a = request, b = freed tokens, x = headroom after
+ *   KV_CACHE_TRANSFER_START  replica = decode dst, a = request, b = reserved tokens,
+ *                            c = prefill src, x = decode pool used after the reservation
+ *                            (pd.py:161-175)
+ *   KV_CACHE_TRANSFER_DONE   replica = decode dst, a = request, c = prefill src
+ *   *_DONE (AF nodes)        a = micro-batch i, b = layer k (both 1-based), c = step,
+ *                            x = node start ns (af.py:177-194)
+ *   TOKEN_EMITTED            replica (request_ids = the batch completing on it at t)
+ *   REQUEST_COMPLETE         replica, a = request                                     */
+enum fs_event_kind {          /* core.py:38-51 EventKind, declaration order */
+  FS_EV_REQUEST_ARRIVAL = 0, FS_EV_BATCH_START = 1, FS_EV_BATCH_COMPLETE = 2,
+  FS_EV_PREFILL_COMPLETE = 3, FS_EV_MEMORY_AVAILABLE = 4, FS_EV_KV_TRANSFER_START = 5,
+  FS_EV_KV_TRANSFER_DONE = 6, FS_EV_ATTN_DONE = 7, FS_EV_A2F_DONE = 8, FS_EV_FFN_DONE = 9,
+  FS_EV_F2A_DONE = 10, FS_EV_TOKEN_EMITTED = 11, FS_EV_REQUEST_COMPLETE = 12
+};
+typedef struct {
+  int64_t t;
+  int64_t seq;
+  int64_t x;
+  int32_t a, b, c;
+  int16_t replica;
+  uint8_t kind;               /* enum fs_event_kind */
+  uint8_t pad;
+} fs_event_rec;               /* 40 bytes */
 
 typedef struct {
   int32_t replica;            /* local replica index */
@@ -285,6 +325,10 @@ typedef struct {
   int32_t* batch_count;       /* per instance */
   int32_t* route_count;
   int32_t* truncated;
+  /* event trace (optional): records indexed by seq; event_count = events scheduled */
+  const int64_t* event_base;  int32_t event_cap; int32_t pad0;
+  fs_event_rec* events;
+  int64_t* event_count;       /* per instance */
 } fs_log;
 
 /* ---- engine lifecycle ---------------------------------------------------- */

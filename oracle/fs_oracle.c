@@ -390,6 +390,7 @@ typedef struct {
   int rep;
   IVec ids;
   int64_t duration_ns;
+  int64_t pool_used;         /* pool.snapshot() at start (base.py:245) */
   int64_t af_step;
   double* moe;               /* per-layer raw ratios or NULL */
   int n_moe;
@@ -447,7 +448,17 @@ static void fail(Sim* s, int status, int detail) {
 static int ev_less(const Ev* a, const Ev* b) {
   return a->t < b->t || (a->t == b->t && a->seq < b->seq);
 }
-static void schedule(Sim* s, int64_t t, int kind, int32_t a, int64_t b) {
+/* event-trace record of a scheduled event, stored at index seq (fs_event_rec) */
+static void otrace(Sim* s, int64_t seq, int64_t t, int kind, int replica, int32_t a, int32_t b,
+                   int32_t c, int64_t x) {
+  fs_log* L = s->log;
+  if (!L || !L->events) return;
+  if (seq >= L->event_cap) { L->truncated[s->inst] = 1; return; }
+  fs_event_rec* r = &L->events[L->event_base[s->inst] + seq];
+  r->t = t; r->seq = seq; r->x = x; r->a = a; r->b = b; r->c = c;
+  r->replica = (int16_t)replica; r->kind = (uint8_t)kind; r->pad = 0;
+}
+static int64_t schedule(Sim* s, int64_t t, int kind, int32_t a, int64_t b) {
   if (t < s->now) fail(s, FS_ERR_SCHEDULING_IN_PAST, kind);
   if (s->hn == s->hcap) {
     s->hcap = s->hcap ? 2 * s->hcap : 64;
@@ -462,6 +473,7 @@ static void schedule(Sim* s, int64_t t, int kind, int32_t a, int64_t b) {
     i = p;
   }
   s->heap[i] = e;
+  return e.seq;
 }
 static Ev heap_pop(Sim* s) {
   Ev top = s->heap[0];
@@ -996,7 +1008,36 @@ static void kick(Sim* s, int ri) {
   if (R->busy || R->start_pending) return;
   if (R->queue.n == 0 && R->running.n == 0) return;
   R->start_pending = 1;
-  schedule(s, s->now, EV_BATCH_START, ri, 0);
+  int64_t sq = schedule(s, s->now, EV_BATCH_START, ri, 0);
+  otrace(s, sq, s->now, EV_BATCH_START, ri, 0, 0, 0, 0);
+}
+
+/* batch record (fs_batch_rec) written when the batch's BATCH_COMPLETE is scheduled */
+static void olog_batch(Sim* s, int bi, int64_t t_complete, int64_t seq, int64_t af_step) {
+  fs_log* log = s->log;
+  Batch* b = &s->batches[bi];
+  if (log && log->events) otrace(s, seq, t_complete, EV_BATCH_COMPLETE, b->rep, bi, 0, 0, 0);
+  if (!log || !log->batches) return;
+  int inst = s->inst;
+  int32_t c = log->batch_count[inst];
+  if (c < log->batch_cap && s->log_moff + b->ids.n <= log->member_cap &&
+      s->log_eoff + b->n_moe <= log->moe_cap) {
+    fs_batch_rec* br = &log->batches[log->batch_base[inst] + c];
+    br->replica = b->rep; br->phase = b->phase; br->t_complete = t_complete;
+    br->duration_ns = b->duration_ns; br->n_members = b->ids.n;
+    br->member_offset = s->log_moff;
+    br->seq = seq; br->pool_used = b->pool_used; br->af_step = af_step;
+    for (int q = 0; q < b->ids.n; q++)
+      log->members[log->member_base[inst] + s->log_moff + q] = b->ids.v[q];
+    s->log_moff += b->ids.n;
+    if (b->n_moe) {
+      br->moe_offset = s->log_eoff; br->n_moe = b->n_moe;
+      for (int q = 0; q < b->n_moe; q++)
+        log->moe_ratio[log->moe_base[inst] + s->log_eoff + q] = b->moe[q];
+      s->log_eoff += b->n_moe;
+    } else { br->moe_offset = -1; br->n_moe = 0; }
+    log->batch_count[inst] = c + 1;
+  } else log->truncated[inst] = 1;
 }
 
 static void start_batch(Sim* s, int ri, int phase, const int32_t* ids, int n) {
@@ -1012,15 +1053,20 @@ static void start_batch(Sim* s, int ri, int phase, const int32_t* ids, int n) {
   s->batches[bi].duration_ns = dur;
   s->batches[bi].moe = moe;
   s->batches[bi].n_moe = moe ? d->num_layers : 0;
-  schedule(s, s->now + dur, EV_BATCH_COMPLETE, ri, bi);
+  s->batches[bi].pool_used = R->pool.used;
+  int64_t sq = schedule(s, s->now + dur, EV_BATCH_COMPLETE, ri, bi);
+  olog_batch(s, bi, s->now + dur, sq, -1);
 }
 
 static void complete_request(Sim* s, int ri, int r) {
   s->done_ns[r] = s->now;
   s->done_rank[r] = s->n_done++;
-  schedule(s, s->now, EV_REQUEST_COMPLETE, ri, r);
-  pool_release(s, &s->rep[ri].pool, r);
-  schedule(s, s->now, EV_MEMORY_AVAILABLE, ri, r);
+  int64_t sq = schedule(s, s->now, EV_REQUEST_COMPLETE, ri, r);
+  otrace(s, sq, s->now, EV_REQUEST_COMPLETE, ri, r, 0, 0, 0);
+  Pool* pl = &s->rep[ri].pool;
+  int64_t freed = pool_release(s, pl, r);
+  sq = schedule(s, s->now, EV_MEMORY_AVAILABLE, ri, r);
+  otrace(s, sq, s->now, EV_MEMORY_AVAILABLE, ri, r, (int32_t)freed, 0, pl->cap - pl->used);
 }
 
 /* build_prefill_batch (cluster.py:145-183); out ids in candidate order */
@@ -1106,10 +1152,12 @@ static void prefill_complete(Sim* s, int ri, const Batch* b, int to_running) {
   for (int i = 0; i < b->ids.n; i++) {
     int r = b->ids.v[i];
     s->emitted[r] += 1;
-    schedule(s, s->now, EV_PREFILL_COMPLETE, ri, r);
+    int64_t sq = schedule(s, s->now, EV_PREFILL_COMPLETE, ri, r);
+    otrace(s, sq, s->now, EV_PREFILL_COMPLETE, ri, r, 0, 0, 0);
   }
   if (b->ids.n) {
-    schedule(s, s->now, EV_TOKEN_EMITTED, ri, -1);
+    int64_t sq = schedule(s, s->now, EV_TOKEN_EMITTED, ri, -1);
+    otrace(s, sq, s->now, EV_TOKEN_EMITTED, ri, 0, 0, 0, 0);
     for (int i = 0; i < b->ids.n; i++)
       if (s->first_ns[b->ids.v[i]] < 0) s->first_ns[b->ids.v[i]] = s->now;
   }
@@ -1122,7 +1170,8 @@ static void prefill_complete(Sim* s, int ri, const Batch* b, int to_running) {
 }
 static int decode_complete(Sim* s, int ri, const Batch* b) {
   Rep* R = &s->rep[ri];
-  schedule(s, s->now, EV_TOKEN_EMITTED, ri, -1);
+  int64_t sq = schedule(s, s->now, EV_TOKEN_EMITTED, ri, -1);
+  otrace(s, sq, s->now, EV_TOKEN_EMITTED, ri, 0, 0, 0, 0);
   for (int i = 0; i < b->ids.n; i++)
     if (s->first_ns[b->ids.v[i]] < 0) s->first_ns[b->ids.v[i]] = s->now;
   int nf = 0;
@@ -1250,16 +1299,21 @@ static void pd_pump(Sim* s) {
     s->transfer_queue.n--;
     s->decode_home[r] = best;
     int64_t nbytes = d->kv_bytes_per_token * s->prompt[r];
-    schedule(s, s->now, EV_KV_START, best, r);
+    int64_t sq = schedule(s, s->now, EV_KV_START, best, r);
+    otrace(s, sq, s->now, EV_KV_START, best, r, (int32_t)D->pool.charged[r], s->prefill_home[r],
+           D->pool.used);
     double sec = d->inter_latency_s + (double)nbytes / d->inter_bandwidth_bps;
     int64_t dur = py_round(sec * 1e9);
-    schedule(s, s->now + dur, EV_KV_DONE, best, r);
+    sq = schedule(s, s->now + dur, EV_KV_DONE, best, r);
+    otrace(s, sq, s->now + dur, EV_KV_DONE, best, r, 0, s->prefill_home[r], 0);
   }
 }
 static void pd_on_transfer_done(Sim* s, int r) {
   int ph = s->prefill_home[r];
-  pool_release(s, &s->rep[ph].pool, r);
-  schedule(s, s->now, EV_MEMORY_AVAILABLE, ph, r);
+  Pool* pl = &s->rep[ph].pool;
+  int64_t freed = pool_release(s, pl, r);
+  int64_t sq = schedule(s, s->now, EV_MEMORY_AVAILABLE, ph, r);
+  otrace(s, sq, s->now, EV_MEMORY_AVAILABLE, ph, r, (int32_t)freed, 0, pl->cap - pl->used);
   int dh = s->decode_home[r];
   iv_push(&s->rep[dh].queue, r);
   kick(s, ph);
@@ -1333,7 +1387,8 @@ static void af_start_node(Sim* s, AfEngine* g, int res) {
   if (!found) { g->pend_t[g->n_pend] = end; g->pend_n[g->n_pend] = 1; g->n_pend++; }
   s->af_busy[res] += dur;
   if (kind == 0) s->af_step_attn[s->n_af - 1] += dur;
-  schedule(s, end, EV_ATTN_DONE + kind, i, dur);
+  int64_t sq = schedule(s, end, EV_ATTN_DONE + kind, i, dur);
+  otrace(s, sq, end, EV_ATTN_DONE + kind, 0, i + 1, k + 1, (int32_t)g->step_id, s->now);
 }
 static void af_dispatch_all(Sim* s, AfEngine* g) {
   for (int res = 0; res < 4; res++)
@@ -1423,7 +1478,9 @@ static void af_on_batch_complete_schedule(Sim* s, AfEngine* g) {
   s->batches[bi].duration_ns = g->final_ts - g->start_ts;
   s->batches[bi].af_step = g->step_id;
   s->af_step_dur[s->n_af - 1] = g->final_ts - g->start_ts;
-  schedule(s, g->final_ts, EV_BATCH_COMPLETE, 0, bi);
+  s->batches[bi].pool_used = s->rep[0].pool.used;
+  int64_t sq = schedule(s, g->final_ts, EV_BATCH_COMPLETE, 0, bi);
+  olog_batch(s, bi, g->final_ts, sq, g->step_id);
   free(g->ids); free(g->mb_size); free(g->stage); free(g->dur); free(g->pend_t); free(g->pend_n);
   free(g);
   s->af = NULL;
@@ -1509,7 +1566,10 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
   if (setjmp(s->jb) == 0) {
     /* learned grouped GEMM on MoE layers needs numpy's np.log (entropy): next */
     /* schedule_arrivals (base.py:167-177): seq 0..N-1 */
-    for (int i = 0; i < N; i++) schedule(s, arrival[i], EV_ARRIVAL, -1, i);
+    for (int i = 0; i < N; i++) {
+      int64_t sq = schedule(s, arrival[i], EV_ARRIVAL, -1, i);
+      otrace(s, sq, arrival[i], EV_ARRIVAL, -1, i, 0, 0, 0);
+    }
     while (s->hn) {
       Ev e = heap_pop(s);
       s->processed++;
@@ -1529,26 +1589,6 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
         case EV_BATCH_COMPLETE: {
           Batch* b = &s->batches[e.b];
           s->rep[e.a].busy_ns += b->duration_ns;
-          if (log && log->batches) {
-            int32_t c = log->batch_count[inst];
-            if (c < log->batch_cap && s->log_moff + b->ids.n <= log->member_cap &&
-                s->log_eoff + b->n_moe <= log->moe_cap) {
-              fs_batch_rec* br = &log->batches[log->batch_base[inst] + c];
-              br->replica = b->rep; br->phase = b->phase; br->t_complete = e.t;
-              br->duration_ns = b->duration_ns; br->n_members = b->ids.n;
-              br->member_offset = s->log_moff;
-              for (int q = 0; q < b->ids.n; q++)
-                log->members[log->member_base[inst] + s->log_moff + q] = b->ids.v[q];
-              s->log_moff += b->ids.n;
-              if (b->n_moe) {
-                br->moe_offset = s->log_eoff; br->n_moe = b->n_moe;
-                for (int q = 0; q < b->n_moe; q++)
-                  log->moe_ratio[log->moe_base[inst] + s->log_eoff + q] = b->moe[q];
-                s->log_eoff += b->n_moe;
-              } else { br->moe_offset = -1; br->n_moe = 0; }
-              log->batch_count[inst] = c + 1;
-            } else log->truncated[inst] = 1;
-          }
           if (b->phase == 0) row->prefill_batches++;
           else if (b->phase == 1) row->decode_batches++;
           else row->af_steps++;
@@ -1575,6 +1615,7 @@ int fso_run_instance(const fs_instance_desc* d, const fs_replica_desc* reps,
       if (s->emitted[i] != output[i]) fail(s, FS_ERR_SIMULATION, i);
   }
 
+  if (log && log->event_count) log->event_count[inst] = s->next_seq;
   row->status = s->status;
   row->status_detail = s->detail;
   row->events = s->processed;
@@ -1925,7 +1966,8 @@ int fso_struct_sizes(int64_t* out, int n) {
                        (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
                        (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
                        (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc),
-                       (int64_t)sizeof(fs_workload_desc)};
+                       (int64_t)sizeof(fs_workload_desc), (int64_t)sizeof(fs_event_rec),
+                       (int64_t)sizeof(fs_log)};
   const int k = (int)(sizeof(s) / sizeof(s[0]));
   for (int i = 0; i < n && i < k; i++) out[i] = s[i];
   return k;

@@ -72,7 +72,17 @@ REPLICA_OUT = np.dtype([("busy_ns", "<i8"), ("busy_fraction", "<f8"),
 
 BATCH_REC = np.dtype([("replica", "<i4"), ("phase", "<i4"), ("t_complete", "<i8"),
                       ("duration_ns", "<i8"), ("n_members", "<i4"), ("member_offset", "<i4"),
-                      ("moe_offset", "<i4"), ("n_moe", "<i4")], align=True)
+                      ("moe_offset", "<i4"), ("n_moe", "<i4"), ("seq", "<i8"),
+                      ("pool_used", "<i8"), ("af_step", "<i8")], align=True)
+
+# fs_event_rec / enum fs_event_kind (core.py:38-51 EventKind order)
+EVENT_REC = np.dtype([("t", "<i8"), ("seq", "<i8"), ("x", "<i8"), ("a", "<i4"), ("b", "<i4"),
+                      ("c", "<i4"), ("replica", "<i2"), ("kind", "u1"), ("pad", "u1")],
+                     align=True)
+EVENT_KINDS = ("REQUEST_ARRIVAL", "BATCH_START", "BATCH_COMPLETE", "PREFILL_COMPLETE",
+               "MEMORY_AVAILABLE", "KV_CACHE_TRANSFER_START", "KV_CACHE_TRANSFER_DONE",
+               "ATTN_COMPUTE_DONE", "A_TO_F_TRANSFER_DONE", "FFN_COMPUTE_DONE",
+               "F_TO_A_TRANSFER_DONE", "TOKEN_EMITTED", "REQUEST_COMPLETE")
 
 ROUTE_REC = np.dtype([("replica", "<i4"), ("micro_batch", "<i4"), ("step", "<i8"),
                       ("layer", "<i4"), ("tokens", "<i4"), ("counts_offset", "<i4"),
@@ -94,7 +104,7 @@ ARRIVAL_KINDS = {"poisson": 0, "fixed_interval": 1, "batch_at_zero": 2}
 LENGTH_KINDS = {"fixed": 0, "uniform": 1, "lognormal": 2}
 
 STRUCT_ORDER = (COST_CTX, SEED_PREFIX, REPLICA_DESC, INSTANCE_DESC, METRIC_ROW, REPLICA_OUT,
-                BATCH_REC, ROUTE_REC, ATTN_PARAMS, FOREST_DESC, WORKLOAD_DESC)
+                BATCH_REC, ROUTE_REC, ATTN_PARAMS, FOREST_DESC, WORKLOAD_DESC, EVENT_REC)
 
 
 class RequestSoA(ctypes.Structure):
@@ -127,6 +137,8 @@ class LogC(ctypes.Structure):
         ("routes", ctypes.c_void_p), ("counts", ctypes.c_void_p),
         ("batch_count", ctypes.c_void_p), ("route_count", ctypes.c_void_p),
         ("truncated", ctypes.c_void_p),
+        ("event_base", ctypes.c_void_p), ("event_cap", ctypes.c_int32), ("pad0", ctypes.c_int32),
+        ("events", ctypes.c_void_p), ("event_count", ctypes.c_void_p),
     ]
 
 
@@ -143,7 +155,7 @@ def check_sizes(lib, fn_name: str) -> None:
     fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
     out = np.zeros(16, dtype=np.int64)
     n = fn(ptr(out), 16)
-    want = [dt.itemsize for dt in STRUCT_ORDER]
+    want = [dt.itemsize for dt in STRUCT_ORDER] + [ctypes.sizeof(LogC)]
     got = out[:n].tolist()
     if got[: len(want)] != want:
         raise RuntimeError(f"ABI struct size mismatch: library {got}, binding {want}")

@@ -140,6 +140,6 @@ def run_one(config: DeploymentConfig, engine: Engine | None = None) -> dict:
                           af=spec.af, routing=spec.routing, seed=spec.seed,
                           attention_model=spec.attention_model,
                           grouped_gemm_model=spec.grouped_gemm_model, engine=engine)
-    result = sim.run()
-    return {"config": config, "trace": result, "metrics": compute_metrics(result),
+    trace = sim.run()
+    return {"config": config, "trace": trace, "metrics": compute_metrics(trace, spec.deployment),
             "config_hash": config.config_hash()}

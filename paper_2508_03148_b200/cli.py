@@ -23,9 +23,32 @@ from .workload import WorkloadError
 CONFIG_ERRORS = (ParseError, ValidationError, TopologyError, WorkloadError, FileNotFoundError)
 
 
+def write_run_artifacts(result: dict, out_dir: str) -> dict[str, str]:
+    """trace.log (body + `#hash=` footer), metrics.json, summary.csv (cli.py:121-141)."""
+    import csv
+    import io
+    from .metrics import SUMMARY_CSV_HEADER, summary_csv_row
+    from .sweep import _atomic_write
+    paths = {"trace": os.path.join(out_dir, "trace.log"),
+             "metrics": os.path.join(out_dir, "metrics.json"),
+             "summary": os.path.join(out_dir, "summary.csv")}
+    trace = result["trace"]
+    body = trace.body_bytes()
+    _atomic_write(paths["trace"], body + f"#hash={trace.hash}\n".encode("utf-8"))
+    doc = result["metrics"].to_dict()
+    doc.update(config_hash=result["config_hash"], seed=result["config"].seed,
+               mode=result["config"].mode)
+    _atomic_write(paths["metrics"], (json.dumps(doc, sort_keys=True, indent=2) + "\n").encode("utf-8"))
+    buf = io.StringIO()
+    w = csv.writer(buf)
+    w.writerow(SUMMARY_CSV_HEADER)
+    w.writerow(summary_csv_row(result["metrics"], result["config_hash"]))
+    _atomic_write(paths["summary"], buf.getvalue().encode("utf-8"))
+    return paths
+
+
 def cmd_run(args) -> int:
     from .api import run_one
-    from .sweep import _atomic_write
     config = load_config(args.config)
     if args.seed is not None:
         wl = config.workload
@@ -34,10 +57,7 @@ def cmd_run(args) -> int:
         config = dataclasses.replace(config, seed=args.seed, workload=wl)
     out_dir = args.out or config.output_dir
     result = run_one(config)
-    doc = result["metrics"].to_dict()
-    doc.update(config_hash=result["config_hash"], seed=config.seed, mode=config.mode)
-    _atomic_write(os.path.join(out_dir, "metrics.json"),
-                  (json.dumps(doc, sort_keys=True, indent=2) + "\n").encode("utf-8"))
+    write_run_artifacts(result, out_dir)
     s = result["metrics"].workload_summary
     print("batch_size,avg_input,output,throughput_tokens_per_s_per_gpu")
     print(f"{s['batch_size']},{s['avg_input_tokens']:g},{s['avg_output_tokens']:g},"

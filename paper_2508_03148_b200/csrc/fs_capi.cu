@@ -51,7 +51,8 @@ struct fs_engine {
   DevBuf rows, rep_out;
   // log mirrors
   DevBuf lg_batch_base, lg_member_base, lg_moe_base, lg_route_base, lg_counts_base, lg_batches,
-      lg_members, lg_moe, lg_routes, lg_counts, lg_bcount, lg_rcount, lg_trunc;
+      lg_members, lg_moe, lg_routes, lg_counts, lg_bcount, lg_rcount, lg_trunc, lg_event_base,
+      lg_events, lg_ecount;
   // cost-model scratch
   DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
       c_layers, c_seeds, c_pf, c_mid, c_scratch;
@@ -103,7 +104,8 @@ int fs_struct_sizes(int64_t* out, int n) {
                        (int64_t)sizeof(fs_metric_row),   (int64_t)sizeof(fs_replica_out),
                        (int64_t)sizeof(fs_batch_rec),    (int64_t)sizeof(fs_route_rec),
                        (int64_t)sizeof(fs_attn_params),  (int64_t)sizeof(fs_forest_desc),
-                       (int64_t)sizeof(fs_workload_desc)};
+                       (int64_t)sizeof(fs_workload_desc), (int64_t)sizeof(fs_event_rec),
+                       (int64_t)sizeof(fs_log)};
   const int k = (int)(sizeof(s) / sizeof(s[0]));
   for (int i = 0; i < n && i < k; i++) out[i] = s[i];
   return k;
@@ -400,7 +402,7 @@ int fs_run_batch(fs_engine* e, const fs_instance_desc* descs, int32_t n_instance
                     trace_counts, n_trace_counts, requests, n_requests);
   if (rc) return rc;
   cudaStream_t s = e->stream;
-  int64_t nb = 0, nm = 0, ne = 0, nro = 0, nc = 0;
+  int64_t nb = 0, nm = 0, ne = 0, nro = 0, nc = 0, nev = 0;
   if (log) {
     // device mirror of the caller's log buffers
     nb = log->batches ? log_total(log->batch_base, n_instances, log->batch_cap) : 0;
@@ -408,10 +410,12 @@ int fs_run_batch(fs_engine* e, const fs_instance_desc* descs, int32_t n_instance
     ne = log->moe_ratio ? log_total(log->moe_base, n_instances, log->moe_cap) : 0;
     nro = log->routes ? log_total(log->route_base, n_instances, log->route_cap) : 0;
     nc = log->counts ? log_total(log->counts_base, n_instances, log->counts_cap) : 0;
+    nev = log->events ? log_total(log->event_base, n_instances, log->event_cap) : 0;
     fs_log& dl = e->params.log;
     memset(&dl, 0, sizeof dl);
     dl.batch_cap = log->batch_cap; dl.member_cap = log->member_cap; dl.moe_cap = log->moe_cap;
     dl.route_cap = log->route_cap; dl.counts_cap = log->counts_cap;
+    dl.event_cap = log->event_cap;
     const int64_t zero = 0;
     (void)zero;
     std::vector<int64_t> zeros(n_instances, 0);
@@ -420,16 +424,25 @@ int fs_run_batch(fs_engine* e, const fs_instance_desc* descs, int32_t n_instance
     FS_CHECK(upload(e->lg_moe_base, log->moe_base ? log->moe_base : zeros.data(), n_instances, s));
     FS_CHECK(upload(e->lg_route_base, log->route_base ? log->route_base : zeros.data(), n_instances, s));
     FS_CHECK(upload(e->lg_counts_base, log->counts_base ? log->counts_base : zeros.data(), n_instances, s));
+    FS_CHECK(upload(e->lg_event_base, log->event_base ? log->event_base : zeros.data(), n_instances, s));
     dl.batch_base = e->lg_batch_base.as<int64_t>();
     dl.member_base = e->lg_member_base.as<int64_t>();
     dl.moe_base = e->lg_moe_base.as<int64_t>();
     dl.route_base = e->lg_route_base.as<int64_t>();
     dl.counts_base = e->lg_counts_base.as<int64_t>();
+    dl.event_base = e->lg_event_base.as<int64_t>();
     if (nb) { FS_CHECK(e->lg_batches.ensure(nb * sizeof(fs_batch_rec))); dl.batches = e->lg_batches.as<fs_batch_rec>(); }
     if (nm) { FS_CHECK(e->lg_members.ensure(nm * 4)); dl.members = e->lg_members.as<int32_t>(); }
     if (ne) { FS_CHECK(e->lg_moe.ensure(ne * 8)); dl.moe_ratio = e->lg_moe.as<double>(); }
     if (nro) { FS_CHECK(e->lg_routes.ensure(nro * sizeof(fs_route_rec))); dl.routes = e->lg_routes.as<fs_route_rec>(); }
     if (nc) { FS_CHECK(e->lg_counts.ensure(nc * 4)); dl.counts = e->lg_counts.as<int32_t>(); }
+    if (nev) {
+      FS_CHECK(e->lg_events.ensure(nev * sizeof(fs_event_rec)));
+      dl.events = e->lg_events.as<fs_event_rec>();
+    }
+    FS_CHECK(e->lg_ecount.ensure(8 * (size_t)std::max(n_instances, 1)));
+    FS_CHECK(cudaMemsetAsync(e->lg_ecount.p, 0, 8 * (size_t)n_instances, s));
+    dl.event_count = e->lg_ecount.as<int64_t>();
     FS_CHECK(e->lg_bcount.ensure(4 * (size_t)std::max(n_instances, 1)));
     FS_CHECK(e->lg_rcount.ensure(4 * (size_t)std::max(n_instances, 1)));
     FS_CHECK(e->lg_trunc.ensure(4 * (size_t)std::max(n_instances, 1)));
@@ -453,6 +466,8 @@ int fs_run_batch(fs_engine* e, const fs_instance_desc* descs, int32_t n_instance
     if (log->batch_count) FS_CHECK(cudaMemcpy(log->batch_count, e->lg_bcount.p, 4 * (size_t)n_instances, cudaMemcpyDeviceToHost));
     if (log->route_count) FS_CHECK(cudaMemcpy(log->route_count, e->lg_rcount.p, 4 * (size_t)n_instances, cudaMemcpyDeviceToHost));
     if (log->truncated) FS_CHECK(cudaMemcpy(log->truncated, e->lg_trunc.p, 4 * (size_t)n_instances, cudaMemcpyDeviceToHost));
+    if (nev) FS_CHECK(cudaMemcpy(log->events, e->lg_events.p, nev * sizeof(fs_event_rec), cudaMemcpyDeviceToHost));
+    if (log->event_count) FS_CHECK(cudaMemcpy(log->event_count, e->lg_ecount.p, 8 * (size_t)n_instances, cudaMemcpyDeviceToHost));
   }
   e->params.log_enabled = 0;
   memset(&e->params.log, 0, sizeof e->params.log);

@@ -982,10 +982,24 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
   return ls.result() + pp;
 }
 
+// ---- optional event trace (fs_event_rec at index seq; one lane writes) ------------------
+__device__ __forceinline__ bool tracing(const EngineParams& P) {
+  return P.log_enabled && P.log.events != nullptr;
+}
+__device__ void trace_put(const EngineParams& P, const Inst& I, int64_t seq, int64_t t, int kind,
+                          int replica, int32_t a, int32_t b, int32_t c, int64_t x) {
+  if (seq >= P.log.event_cap) { P.log.truncated[I.idx] = 1; return; }
+  fs_event_rec r;
+  r.t = t; r.seq = seq; r.x = x; r.a = a; r.b = b; r.c = c;
+  r.replica = (int16_t)replica; r.kind = (uint8_t)kind; r.pad = 0;
+  P.log.events[P.log.event_base[I.idx] + seq] = r;
+}
+
 // ---- optional batch log -------------------------------------------------------------------
-// A batch's moe-ratio slot is reserved when it starts: several replicas can have
-// batches in flight, so slots are handed out in start order and each batch
-// record points at its own. Returns offset + 1 (0 = not logged).
+// A batch is recorded when it starts (members, duration, pool snapshot, the seq of
+// its BATCH_COMPLETE); its moe-ratio slot is reserved then too. Records are in
+// start order; the host sorts by (t_complete, seq) for completion order.
+// log_moe_reserve returns offset + 1 (0 = not logged).
 __device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
   if (!P.log_enabled || !P.log.batches || !I.d->has_moe) return 0;
   if (I.log_eoff + I.d->num_layers > P.log.moe_cap) return 0;
@@ -993,29 +1007,44 @@ __device__ int32_t log_moe_reserve(const EngineParams& P, Inst& I) {
   I.log_eoff += I.d->num_layers;
   return off + 1;
 }
-__device__ void log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
-                          const int32_t* members, int nm, int32_t moe_off1) {
-  if (!P.log_enabled || !P.log.batches) return;
+__device__ int32_t log_batch(const EngineParams& P, Inst& I, int r, int phase, int64_t dur,
+                             const int32_t* members, int nm, int32_t moe_off1, int64_t pool_used,
+                             int64_t af_step) {
+  if (!P.log_enabled || !P.log.batches) return -1;
   const int n_moe = moe_off1 ? I.d->num_layers : 0;
   const bool need_moe = I.d->has_moe && phase != PH_AF;
   const int32_t c = I.log_batches;
   if (c < P.log.batch_cap && I.log_moff + nm <= P.log.member_cap && (!need_moe || moe_off1)) {
     if (I.lane == 0) {
       fs_batch_rec rec;
-      rec.replica = r; rec.phase = phase; rec.t_complete = I.now; rec.duration_ns = dur;
+      rec.replica = r; rec.phase = phase; rec.t_complete = I.now + dur; rec.duration_ns = dur;
       rec.n_members = nm; rec.member_offset = I.log_moff;
       rec.moe_offset = n_moe ? moe_off1 - 1 : -1;
       rec.n_moe = n_moe;
+      rec.seq = I.seq;  // the BATCH_COMPLETE about to be scheduled
+      rec.pool_used = pool_used;
+      rec.af_step = af_step;
       P.log.batches[P.log.batch_base[I.idx] + c] = rec;
     }
     const int64_t mb = P.log.member_base[I.idx] + I.log_moff;
     for (int i = I.lane; i < nm; i += 32) P.log.members[mb + i] = members[i];
     I.log_moff += nm;
     I.log_batches = c + 1;
-  } else if (I.lane == 0) {
-    P.log.truncated[I.idx] = 1;
+    __syncwarp();
+    return c;
   }
+  if (I.lane == 0) P.log.truncated[I.idx] = 1;
   __syncwarp();
+  return -1;
+}
+
+// BATCH_COMPLETE at now + dur: batch record + trace record, then the heap event
+__device__ void schedule_batch_complete(const EngineParams& P, Inst& I, int r, int phase,
+                                        int64_t dur, const int32_t* members, int nm,
+                                        int32_t moe_off1, int64_t pool_used, int64_t af_step) {
+  const int32_t bi = log_batch(P, I, r, phase, dur, members, nm, moe_off1, pool_used, af_step);
+  if (tracing(P) && I.lane == 0)
+    trace_put(P, I, I.seq, I.now + dur, FS_EV_BATCH_COMPLETE, r, bi, 0, 0, 0);
 }
 
 // ---- list helpers ---------------------------------------------------------------------------
@@ -1189,6 +1218,9 @@ __device__ void launch_batch(const EngineParams& P, Inst& I, int r, RepState& s,
   s.inflight_phase = phase;
   s.inflight_dur = dur;
   s.inflight_moe = moe_off1;
+  if (P.log_enabled)
+    schedule_batch_complete(P, I, r, phase, dur, phase == PH_PREFILL ? ilist(I, r) : rlist(I, r),
+                            phase == PH_PREFILL ? s.ilen : s.rlen, moe_off1, s.used, -1);
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, r, dur);
 }
 
@@ -1247,10 +1279,11 @@ __device__ void start_decode(const EngineParams& P, Inst& I, int r, RepState& s,
   launch_batch(P, I, r, s, rd, b, PH_DECODE, sm);
 }
 
-__device__ void kick(Inst& I, int r, RepState& s) {
+__device__ void kick(const EngineParams& P, Inst& I, int r, RepState& s) {
   if (s.busy || s.start_pending) return;
   if (s.qlen == 0 && s.rlen == 0) return;
   s.start_pending = 1;
+  if (tracing(P) && I.lane == 0) trace_put(P, I, I.seq, I.now, FS_EV_BATCH_START, r, 0, 0, 0, 0);
   heap_push(I, I.now, K_BATCH_START, r, 0);
 }
 
@@ -1284,6 +1317,13 @@ __device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState
   const int nm = s.ilen;
   const unsigned lt = (1u << I.lane) - 1u;
   I.events += nm + 1;  // PREFILL_COMPLETE per member + one TOKEN_EMITTED
+  // sequence numbers (colocated.py:75-91): PREFILL_COMPLETE per member, TOKEN_EMITTED,
+  // then REQUEST_COMPLETE + MEMORY_AVAILABLE per finished member, in member order
+  const int64_t seq0 = I.seq;
+  const bool tr = tracing(P);
+  int nf = 0;
+  if (tr && I.lane == 0)
+    trace_put(P, I, seq0 + nm, I.now, FS_EV_TOKEN_EMITTED, r, 0, 0, 0, 0);
   for (int base = 0; base < nm; base += 32) {
     const int i = base + I.lane;
     const bool valid = i < nm;
@@ -1295,12 +1335,24 @@ __device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState
     // completions and appends interleave in member order; they touch disjoint state
     const int64_t fp = fin ? (to_running ? (int64_t)P.prompt[gi(I, req)] + out
                                          : (int64_t)P.prompt[gi(I, req)]) : 0;
-    s.used -= warp_sum_i64(fin ? pool_rounded(d, fp) : 0);
+    const int64_t freed = fin ? pool_rounded(d, fp) : 0;
+    if (tr) {
+      const int64_t used_after = s.used - warp_incl_scan_i64(freed, I.lane);
+      if (valid) trace_put(P, I, seq0 + i, I.now, FS_EV_PREFILL_COMPLETE, r, req, 0, 0, 0);
+      if (fin) {
+        const int64_t sq = seq0 + nm + 1 + 2 * (nf + __popc(fm & lt));
+        trace_put(P, I, sq, I.now, FS_EV_REQUEST_COMPLETE, r, req, 0, 0, 0);
+        trace_put(P, I, sq + 1, I.now, FS_EV_MEMORY_AVAILABLE, r, req, (int32_t)freed, 0,
+                  P.reps[I.rb + r].kv_pool_tokens - used_after);
+      }
+    }
+    s.used -= warp_sum_i64(freed);
     if (fin) {
       P.done_ns[gi(I, req)] = I.now;
       P.done_rank[gi(I, req)] = I.n_done + __popc(fm & lt);
     }
     I.n_done += __popc(fm);
+    nf += __popc(fm);
     I.events += 2 * __popc(fm);
     const bool keep = valid && !fin;
     if (to_running) {
@@ -1312,6 +1364,7 @@ __device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState
     }
     __syncwarp();
   }
+  I.seq = seq0 + nm + 1 + 2 * nf;
 }
 
 // decode / AF completion: every member emitted one token; finished requests leave
@@ -1320,6 +1373,12 @@ __device__ void prefill_complete(const EngineParams& P, Inst& I, int r, RepState
 __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& s) {
   const fs_instance_desc* d = I.d;
   I.events += 1;  // TOKEN_EMITTED
+  // sequence numbers (colocated.py:92-107): TOKEN_EMITTED, then REQUEST_COMPLETE +
+  // MEMORY_AVAILABLE per finished member in running order
+  const int64_t seq0 = I.seq;
+  const bool tr = tracing(P);
+  if (tr && I.lane == 0) trace_put(P, I, seq0, I.now, FS_EV_TOKEN_EMITTED, r, 0, 0, 0, 0);
+  I.seq = seq0 + 1;
   s.dstep++;
   s.sum_ctx += s.rlen;
   if (s.min_finish != s.dstep) return 0;
@@ -1327,6 +1386,7 @@ __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& 
   const unsigned lt = (1u << I.lane) - 1u;
   int w = 0, nf = 0;
   int64_t freed_ctx = 0, freed_pool = 0, new_min = kNoFinish;
+  int64_t freed_run = 0;  // pool tokens released by earlier chunks (tracing only)
   for (int base = 0; base < s.rlen; base += 32) {
     const int i = base + I.lane;
     const bool valid = i < s.rlen;
@@ -1335,6 +1395,17 @@ __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& 
     const bool fin = valid && f == s.dstep;
     const unsigned fm = __ballot_sync(FS_FULL, fin);
     const unsigned km = __ballot_sync(FS_FULL, valid && !fin);
+    if (tr) {
+      const int64_t fr = fin ? pool_rounded(d, (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)]) : 0;
+      const int64_t incl = warp_incl_scan_i64(fr, I.lane);
+      if (fin) {
+        const int64_t sq = seq0 + 1 + 2 * (nf + __popc(fm & lt));
+        trace_put(P, I, sq, I.now, FS_EV_REQUEST_COMPLETE, r, req, 0, 0, 0);
+        trace_put(P, I, sq + 1, I.now, FS_EV_MEMORY_AVAILABLE, r, req, (int32_t)fr, 0,
+                  P.reps[I.rb + r].kv_pool_tokens - (s.used - freed_run - incl));
+      }
+      freed_run += warp_sum_i64(fr);
+    }
     if (fin) {
       const int64_t fp = (int64_t)P.prompt[gi(I, req)] + P.output[gi(I, req)];
       freed_ctx += fp;
@@ -1356,6 +1427,7 @@ __device__ int decode_complete(const EngineParams& P, Inst& I, int r, RepState& 
   s.used -= warp_sum_i64(freed_pool);
   s.min_finish = (int32_t)warp_min_i64(new_min);
   I.events += 2 * nf;
+  I.seq = seq0 + 1 + 2 * nf;
   return nf;
 }
 
@@ -1365,7 +1437,7 @@ __device__ void co_arrival(const EngineParams& P, Inst& I, int req) {
   I.rr++;
   RepState s = load_rep(P, I, r);
   enqueue(P, I, r, s, req);
-  kick(I, r, s);
+  kick(P, I, r, s);
   store_rep(P, I, r, s);
 }
 
@@ -1396,15 +1468,13 @@ __device__ void co_batch_complete(const EngineParams& P, Inst& I, int r, int64_t
   s.busy = 0;
   s.busy_ns += dur;
   if (s.inflight_phase == PH_PREFILL) {
-    log_batch(P, I, r, PH_PREFILL, dur, ilist(I, r), s.ilen, s.inflight_moe);
     I.prefill_batches++;
     prefill_complete(P, I, r, s, true);
   } else {
-    log_batch(P, I, r, s.inflight_phase, dur, rlist(I, r), s.rlen, s.inflight_moe);
     if (s.inflight_phase == PH_AF) I.af_steps++; else I.decode_batches++;
     decode_complete(P, I, r, s);
   }
-  kick(I, r, s);
+  kick(P, I, r, s);
   store_rep(P, I, r, s);
 }
 
@@ -1439,7 +1509,7 @@ __device__ void pd_arrival(const EngineParams& P, Inst& I, int req) {
   if (I.lane == 0) P.home[gi(I, req)] = r;
   enqueue(P, I, r, s, req);
   s.outstanding += P.prompt[gi(I, req)];
-  kick(I, r, s);
+  kick(P, I, r, s);
   store_rep(P, I, r, s);
 }
 
@@ -1461,7 +1531,14 @@ __device__ void pd_pump(const EngineParams& P, Inst& I) {
     I.events += 1;  // KV_CACHE_TRANSFER_START
     const int64_t nbytes = d->kv_bytes_per_token * prompt;
     const double sec = d->inter_latency_s + i2d(nbytes) / d->inter_bandwidth_bps;
-    heap_push(I, I.now + py_round(sec * 1e9), K_KV_DONE, r, req);
+    const int64_t t_done = I.now + py_round(sec * 1e9);
+    if (tracing(P) && I.lane == 0) {
+      const int32_t src = P.home[gi(I, req)];
+      trace_put(P, I, I.seq, I.now, FS_EV_KV_TRANSFER_START, r, req, (int32_t)fp, src, s.used);
+      trace_put(P, I, I.seq + 1, t_done, FS_EV_KV_TRANSFER_DONE, r, req, 0, src, 0);
+    }
+    I.seq++;
+    heap_push(I, t_done, K_KV_DONE, r, req);
   }
 }
 
@@ -1502,20 +1579,18 @@ __device__ void pd_batch_complete(const EngineParams& P, Inst& I, int r, int64_t
   s.busy = 0;
   s.busy_ns += dur;
   if (s.inflight_phase == PH_PREFILL) {
-    log_batch(P, I, r, PH_PREFILL, dur, ilist(I, r), s.ilen, s.inflight_moe);
     I.prefill_batches++;
     prefill_complete(P, I, r, s, false);
     store_rep(P, I, r, s);
     pd_pump(P, I);
   } else {
-    log_batch(P, I, r, PH_DECODE, dur, rlist(I, r), s.rlen, s.inflight_moe);
     I.decode_batches++;
     const int nf = decode_complete(P, I, r, s);
     store_rep(P, I, r, s);
     if (nf) pd_pump(P, I);
   }
   s = load_rep(P, I, r);
-  kick(I, r, s);
+  kick(P, I, r, s);
   store_rep(P, I, r, s);
 }
 
@@ -1525,7 +1600,12 @@ __device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req
   __syncwarp();
   const int ph = P.home[gi(I, req)];
   RepState sp = load_rep(P, I, ph);
-  sp.used -= pool_rounded(d, P.prompt[gi(I, req)]);
+  const int64_t freed = pool_rounded(d, P.prompt[gi(I, req)]);
+  sp.used -= freed;
+  if (tracing(P) && I.lane == 0)
+    trace_put(P, I, I.seq, I.now, FS_EV_MEMORY_AVAILABLE, ph, req, (int32_t)freed, 0,
+              P.reps[I.rb + ph].kv_pool_tokens - sp.used);
+  I.seq++;
   store_rep(P, I, ph, sp);
   RepState sd = load_rep(P, I, dr);
   __syncwarp();
@@ -1533,10 +1613,10 @@ __device__ void pd_transfer_done(const EngineParams& P, Inst& I, int dr, int req
   sd.qlen++;
   store_rep(P, I, dr, sd);
   sp = load_rep(P, I, ph);
-  kick(I, ph, sp);
+  kick(P, I, ph, sp);
   store_rep(P, I, ph, sp);
   sd = load_rep(P, I, dr);
-  kick(I, dr, sd);
+  kick(P, I, dr, sd);
   store_rep(P, I, dr, sd);
 }
 
@@ -1647,7 +1727,9 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
   // list scheduling over 4 exclusive resources; lowest micro-batch claims first;
   // all completions at an instant are retired before dispatch (af.py:141-229)
   int64_t final_ts = 0, attn_busy = 0, busy4[4] = {0, 0, 0, 0};
+  const bool tr = tracing(P);
   if (I.lane == 0) {
+    int64_t nseq = I.seq;  // X_DONE events take seqs in dispatch order (af.py:177-201)
     for (int i = 0; i < m; i++) sm->af_stage[i] = 0;
     unsigned long long ready[4] = {0, 0, 0, 0};
     ready[0] = (m == 64) ? ~0ull : ((1ull << m) - 1ull);
@@ -1668,6 +1750,10 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
           busy_mb[res] = i;
           endt[res] = t + dur;
           busy4[res] += dur;
+          if (tr)
+            trace_put(P, I, nseq, I.now + t + dur, FS_EV_ATTN_DONE + res, 0, i + 1, k + 1,
+                      (int32_t)step, I.now + t);
+          nseq++;
         }
       }
       bool any = false;
@@ -1705,11 +1791,13 @@ __device__ void af_start_step(const EngineParams& P, Inst& I, RepState& s, const
     I.bubble_total += dur;
   }
   I.events += 4LL * m * L - m;  // node-completion events
+  I.seq += 4LL * m * L - m;
   s.busy = 1;
   s.steps++;
   s.inflight_phase = PH_AF;
   s.inflight_dur = dur;
   s.inflight_moe = 0;
+  if (P.log_enabled) schedule_batch_complete(P, I, 0, PH_AF, dur, rl, B, 0, s.used, step);
   heap_push(I, I.now + dur, K_BATCH_COMPLETE, 0, dur);
 }
 
@@ -1756,7 +1844,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
   }
   I.hn = 0;
   I.now = 0;
-  I.seq = 0;
+  I.seq = I.N;  // arrivals hold seq 0..N-1 (base.py:167-177)
   I.events = 0;
   I.max_events = d->max_events;
   I.rr = 0; I.n_done = 0; I.cursor = 0;
@@ -1807,6 +1895,8 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
     if (have_arr && ta <= te) {
       I.now = ta;
       const int req = I.cursor++;
+      if (tracing(P) && lane == 0)
+        trace_put(P, I, req, ta, FS_EV_REQUEST_ARRIVAL, -1, req, 0, 0, 0);
       if (I.mode == FS_MODE_PD) pd_arrival(P, I, req);
       else co_arrival(P, I, req);
     } else {
@@ -1847,6 +1937,7 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
     if (P.log_enabled) {
       if (P.log.batch_count) P.log.batch_count[idx] = I.log_batches;
       if (P.log.route_count) P.log.route_count[idx] = I.log_routes;
+      if (P.log.event_count) P.log.event_count[idx] = I.seq;
     }
     if (P.inst_cycles) P.inst_cycles[idx] = clock64() - t_start;
   }

@@ -71,7 +71,7 @@ def load_library(path: str = LIB_PATH):
         fn.restype = res
         fn.argtypes = args
     abi.check_sizes(lib, "fs_struct_sizes")
-    if lib.fs_abi_version() != 1:
+    if lib.fs_abi_version() != 2:
         raise EngineUnavailable("ABI version mismatch")
     _lib = lib
     return lib
@@ -92,13 +92,14 @@ def attn_params(num_query_heads, num_kv_heads, head_dim, dtype_bytes, peak_flops
 
 @dataclass
 class LogSpec:
-    """Per-instance capacities of the optional batch / routing log."""
+    """Per-instance capacities of the optional batch / routing / event-trace log."""
 
     batch_cap: int = 0
     member_cap: int = 0
     moe_cap: int = 0
     route_cap: int = 0
     counts_cap: int = 0
+    event_cap: int = 0
 
 
 @dataclass
@@ -113,12 +114,19 @@ class RawLog:
     route_count: np.ndarray
     truncated: np.ndarray
     c_struct: abi.LogC
+    events: np.ndarray | None = None
+    event_count: np.ndarray | None = None
 
     def instance_batches(self, i: int) -> list[dict]:
+        """Batch records of instance i in BATCH_COMPLETE dispatch order (t_complete, seq);
+        the engine records them when they start. `index` = position in the raw log."""
         s = self.spec
+        n = int(self.batch_count[i])
+        raw = self.batches[i * s.batch_cap: i * s.batch_cap + n]
+        order = np.lexsort((raw["seq"], raw["t_complete"])) if n else []
         out = []
-        for j in range(int(self.batch_count[i])):
-            b = self.batches[i * s.batch_cap + j]
+        for j in order:
+            b = raw[j]
             mo = int(b["member_offset"])
             mem = self.members[i * s.member_cap + mo: i * s.member_cap + mo + int(b["n_members"])]
             moe = None
@@ -127,8 +135,18 @@ class RawLog:
                 moe = self.moe[eo: eo + int(b["n_moe"])].tolist()
             out.append({"replica": int(b["replica"]), "phase": abi.PHASES[int(b["phase"])],
                         "t_complete": int(b["t_complete"]), "duration_ns": int(b["duration_ns"]),
-                        "members": mem.tolist(), "moe_ratio": moe})
+                        "members": mem.tolist(), "moe_ratio": moe, "seq": int(b["seq"]),
+                        "pool_used": int(b["pool_used"]), "af_step": int(b["af_step"]),
+                        "index": int(j)})
         return out
+
+    def instance_events(self, i: int) -> np.ndarray:
+        """Event records of instance i indexed by seq (fs_event_rec)."""
+        cap = self.spec.event_cap
+        n = int(self.event_count[i])
+        if n > cap:
+            raise RuntimeError(f"event log of instance {i} truncated ({n} events, cap {cap})")
+        return self.events[i * cap: i * cap + n].copy()
 
     def instance_routes(self, i: int) -> list[dict]:
         s = self.spec
@@ -156,12 +174,18 @@ def make_log(n_instances: int, spec: LogSpec) -> RawLog:
         batch_count=np.zeros(n_instances, dtype=np.int32),
         route_count=np.zeros(n_instances, dtype=np.int32),
         truncated=np.zeros(n_instances, dtype=np.int32),
-        c_struct=abi.LogC())
+        c_struct=abi.LogC(),
+        events=np.zeros(max(1, n_instances * spec.event_cap), dtype=abi.EVENT_REC),
+        event_count=np.zeros(n_instances, dtype=np.int64))
     c = log.c_struct
     log._keep = [bases(spec.batch_cap), bases(spec.member_cap), bases(spec.moe_cap),
-                 bases(spec.route_cap), bases(spec.counts_cap)]
+                 bases(spec.route_cap), bases(spec.counts_cap), bases(spec.event_cap)]
+    c.event_base = abi.ptr(log._keep[5])
+    c.event_cap = spec.event_cap
+    c.events = abi.ptr(log.events) if spec.event_cap else None
+    c.event_count = abi.ptr(log.event_count)
     c.batch_base, c.member_base, c.moe_base, c.route_base, c.counts_base = [
-        abi.ptr(b) for b in log._keep]
+        abi.ptr(b) for b in log._keep[:5]]
     c.batch_cap, c.member_cap, c.moe_cap = spec.batch_cap, spec.member_cap, spec.moe_cap
     c.route_cap, c.counts_cap = spec.route_cap, spec.counts_cap
     c.batches = abi.ptr(log.batches) if spec.batch_cap else None

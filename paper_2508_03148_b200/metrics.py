@@ -73,6 +73,18 @@ class InstanceResult:
     batches: list[dict] | None = None
     routes: list[dict] | None = None
     log_truncated: bool = False
+    pool_capacity: list[int] | None = None   # per replica (topology.py:289-302)
+    has_moe: bool = False
+    kv_bytes_per_token: int = 0
+    af_micro_batches: int = 0
+    event_log: np.ndarray | None = None      # fs_event_rec by seq (trace runs only)
+
+    def trace(self):
+        """The reference's EventTrace of this run (needs a run with an event log)."""
+        from .trace import EventTrace
+        if self.event_log is None:
+            raise ValueError("this run did not record an event trace")
+        return EventTrace(self, self.event_log)
 
     @property
     def status(self) -> int:
@@ -121,13 +133,18 @@ def split_results(low, raw, modes: list[str]) -> list[InstanceResult]:
             arrival_ns=low.arrival[o:o + n], prompt=low.prompt[o:o + n],
             output=low.output[o:o + n], first_token_ns=raw.first_ns[o:o + n],
             done_ns=raw.done_ns[o:o + n], completion_rank=raw.done_rank[o:o + n],
-            total_gpus=int(d["total_gpus"]), mode=modes[i])
+            total_gpus=int(d["total_gpus"]), mode=modes[i],
+            pool_capacity=low.replicas["kv_pool_tokens"][ro:ro + nr].tolist(),
+            has_moe=bool(d["has_moe"]), kv_bytes_per_token=int(d["kv_bytes_per_token"]),
+            af_micro_batches=int(d["af_micro_batches"]))
         if raw.log is not None:
             if raw.log.spec.batch_cap:
                 res.batches = raw.log.instance_batches(i)
             if raw.log.spec.route_cap:
                 res.routes = raw.log.instance_routes(i)
             res.log_truncated = bool(raw.log.truncated[i])
+            if raw.log.spec.event_cap and res.ok and not res.log_truncated:
+                res.event_log = raw.log.instance_events(i)
         out.append(res)
     return out
 
@@ -142,12 +159,16 @@ def _agg(v) -> dict[str, float] | None:
     return {"mean": float(v[0]), "p50": float(v[1]), "p90": float(v[2]), "p99": float(v[3])}
 
 
-def compute_metrics(result: InstanceResult, deployment=None) -> MetricsBundle:
+def compute_metrics(result, deployment=None) -> MetricsBundle:
     """MetricsBundle of a device run (reference: metrics.py:81-178).
 
+    `result` is an InstanceResult or the EventTrace `Simulation.run()` returns.
     All reductions were done on the device; per-request values are the
     reference's own expressions over the device's integer timestamps.
     """
+    result = getattr(result, "result", result)  # EventTrace -> InstanceResult
+    if len(result.request_ids) == 0:
+        raise IncompleteTrace("trace contains no requests")  # metrics.py:88-89
     if not result.ok:
         raise IncompleteTrace(str(result.error()))
     row = result.row

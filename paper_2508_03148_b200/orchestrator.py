@@ -3,10 +3,11 @@
 `make_simulation(mode, deployment, requests, policy, ...)` keeps the
 reference's signature (orchestrator/__init__.py:43-50, base.py:71-81); the
 returned object's `run()` executes the whole per-iteration event loop on the
-GPU engine and returns an `InstanceResult` -- the stand-in for the
-reference's EventTrace that `compute_metrics` consumes. Requests passed in
-are updated in place with their final lifecycle (tokens emitted, COMPLETE,
-state timestamps), as the reference's handlers leave them.
+GPU engine and returns the run's `EventTrace` (trace.py: the reference's
+records, lines, sha256 hash and export, rendered from the device's event
+log), which `compute_metrics` consumes. Requests passed in are updated in
+place with their final lifecycle (tokens emitted, COMPLETE, state
+timestamps), as the reference's handlers leave them.
 """
 
 from __future__ import annotations
@@ -18,6 +19,7 @@ from .errors import RequestCannotFit, SimulationError  # noqa: F401  (re-exporte
 from .lower import InstanceSpec, lower
 from .metrics import InstanceResult, split_results
 from .specs import AfPipelineConfig, RoutingPolicySpec
+from .trace import EventTrace
 from .topology import Deployment
 from .workload import Request, RequestArrays, RequestState, arrays_from_requests
 
@@ -26,18 +28,26 @@ __all__ = ["AfPipelineConfig", "RoutingPolicySpec", "make_simulation", "Simulati
            "RequestCannotFit", "detail_log_spec"]
 
 
-def detail_log_spec(spec: InstanceSpec, routes: bool = False) -> LogSpec:
-    """Log capacities large enough for one instance's full batch log.
+def detail_log_spec(spec: InstanceSpec, routes: bool = False, events: bool = False) -> LogSpec:
+    """Log capacities large enough for one instance's full batch log (and event trace).
 
     Every batch emits at least one token and every member emits exactly one,
     so both the batch count and the membership total are bounded by the
-    output-token total.
+    output-token total. Events: N arrivals, PREFILL_COMPLETE, REQUEST_COMPLETE,
+    two MEMORY_AVAILABLE and two KV-transfer events per request; per batch one
+    BATCH_COMPLETE and one TOKEN_EMITTED; one BATCH_START per kick (<= one per
+    arrival, batch completion and transfer completion); 4mL - m node events per
+    AF step.
     """
     tokens = int(spec.requests.output.sum()) + 1
     model = spec.deployment.model
     L = model.num_layers
     moe = model.moe is not None
     log = LogSpec(batch_cap=tokens, member_cap=tokens, moe_cap=tokens * L if moe else 0)
+    if events:
+        n = len(spec.requests.output)
+        per_step = 4 * spec.af.micro_batches * L if (spec.af and spec.deployment.mode == "af") else 0
+        log.event_cap = 10 * n + tokens * (3 + per_step) + 16
     if routes and moe:
         m = spec.af.micro_batches if (spec.af and spec.deployment.mode == "af") else 1
         log.route_cap = tokens * L * max(1, m)
@@ -72,15 +82,16 @@ class Simulation:
         self.log_routes = log_routes
         self.result: InstanceResult | None = None
 
-    def run(self) -> InstanceResult:
+    def run(self) -> EventTrace:
+        """Simulate on the device; returns the EventTrace (base.py:220-229)."""
         eng = self._engine or default_engine()
         low = lower([self.spec])
-        raw = eng.run(low, log=detail_log_spec(self.spec, routes=self.log_routes))
+        raw = eng.run(low, log=detail_log_spec(self.spec, routes=self.log_routes, events=True))
         res = split_results(low, raw, [self.mode])[0]
         self.result = res
         self._update_requests(res)
         res.raise_for_status()
-        return res
+        return res.trace()
 
     def _update_requests(self, res: InstanceResult) -> None:
         for i, req in enumerate(self.requests):

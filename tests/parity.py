@@ -17,14 +17,15 @@ def specs_for(docs, base_dir="."):
     return [instance_spec(parse_config(copy.deepcopy(d), base_dir=base_dir)) for d in docs]
 
 
-def run_backend(backend, docs, routes=False, threads=1, base_dir="."):
-    """backend: 'oracle' or an Engine."""
+def run_backend(backend, docs, routes=False, threads=1, base_dir=".", events=True):
+    """backend: 'oracle' or an Engine. events: also record the event trace."""
     specs = specs_for(docs, base_dir)
     low = lower(specs)
-    logs = [detail_log_spec(s, routes=routes) for s in specs]
+    logs = [detail_log_spec(s, routes=routes, events=events) for s in specs]
     from paper_2508_03148_b200.engine import LogSpec
     log = LogSpec(*(max(getattr(l, f) for l in logs) for f in
-                    ("batch_cap", "member_cap", "moe_cap", "route_cap", "counts_cap")))
+                    ("batch_cap", "member_cap", "moe_cap", "route_cap", "counts_cap",
+                     "event_cap")))
     if backend == "oracle":
         from oracle import oracle
         raw = oracle.run(low, log=log, threads=threads)
@@ -60,6 +61,11 @@ def compare_to_golden(res, g, check_routes=True):
         bad.append(f"iterations {res.iterations} != {g['iterations']}")
     if res.events != g["events"]:
         bad.append(f"events {res.events} != {g['events']}")
+    if "trace_hash" in g and res.event_log is not None:
+        if len(res.event_log) != res.events:
+            bad.append(f"event log has {len(res.event_log)} records, {res.events} events")
+        elif res.trace().hash != g["trace_hash"]:
+            bad.append("trace hash differs")
     if "batches" in g and res.batches is not None:
         gb = g["batches"]
         if len(res.batches) != len(gb):

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version():
     if not os.path.exists(engine.LIB_PATH):
         pytest.skip("engine library not built")
-    assert engine.load_library().fs_abi_version() == 1
+    assert engine.load_library().fs_abi_version() == 2
 
 
 def test_engine_fails_loudly_without_gpu():

@@ -129,7 +129,8 @@ def test_struct_layouts_are_c_layouts():
     assert abi.COST_CTX.itemsize == 40
     assert abi.SEED_PREFIX.itemsize == 232
     assert abi.REPLICA_DESC.itemsize == 64
-    assert abi.BATCH_REC.itemsize == 40
+    assert abi.BATCH_REC.itemsize == 64
+    assert abi.EVENT_REC.itemsize == 40
     assert abi.ROUTE_REC.itemsize == 32
 
 
