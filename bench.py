@@ -13,9 +13,12 @@ batch, decode step or AF step), counted by the engine.
          H2D of descriptors + request SoA, both kernels, D2H of metric rows,
          replica rows and per-request times, wall clock.
 
-Multi-GPU (torchrun): one process per GPU, each simulating its own 4,096
-instances (weak scaling; disjoint seeds), then one NCCL all-gather of the
-fixed-size metric rows. `--impl reference` times the CPU port of the
+Multi-GPU (torchrun): one process per GPU.
+  --scaling weak (default): each rank simulates its own 4,096 instances
+         (disjoint seeds), then one NCCL all-gather of the fixed-size metric rows.
+  --scaling strong: ONE 4,096-instance sweep LPT-sharded over the ranks by
+         api.config_cost (the product path's sharding, api.shard_plan); e2e
+         includes the NCCL all-gather of the rows every step. `--impl reference` times the CPU port of the
 reference path (oracle/fs_oracle.c, all host threads) on a bounded sample of
 the same workload.
 """
@@ -53,6 +56,7 @@ def parse_args():
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config (C1/C3/C4) batches")
     ap.add_argument("--cpu-sample-seeds", type=int, default=8)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     return ap.parse_args()
 
 
@@ -367,7 +371,14 @@ def main():
     from paper_2508_03148_b200.engine import Engine
 
     t_low0 = time.perf_counter()
-    docs = workload_docs(rank, args.seeds, args.requests)
+    strong = args.scaling == "strong"
+    if strong:  # one fixed sweep, LPT-sharded like api.simulate / simulate_rows
+        from paper_2508_03148_b200.api import shard_plan
+        all_docs = workload_docs(0, args.seeds, args.requests)
+        _, shards = shard_plan(all_docs, world)
+        docs = [all_docs[i] for i in shards[rank]]
+    else:
+        docs = workload_docs(rank, args.seeds, args.requests)
     low = lower_docs(docs)
     t_low = time.perf_counter() - t_low0
     eng = Engine(local)
@@ -418,7 +429,9 @@ def main():
     # (events around each phase of one extra launch are not possible inside the
     # library; the ncu launch list in profiles/ gives the split).
 
-    # end-to-end through the C ABI with host buffers (H2D + kernels + D2H)
+    # end-to-end through the C ABI with host buffers (H2D + kernels + D2H); in strong
+    # scaling also the all-gather of every rank's metric rows (the sweep's result)
+    from paper_2508_03148_b200.distributed import gather_rows
     e2e_times = []
     raw = None
     for i in range(args.warmup + args.steps):
@@ -426,9 +439,15 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         raw = eng.run(low)
+        if strong and world > 1:
+            gathered = gather_rows(raw.rows, world, cdev if backend == "nccl" else None)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_times.append(dt)
+    if strong and world > 1:
+        got = sum(int(g["iterations"].sum()) for g in gathered)
+        if got * args.steps != int(total_its):
+            raise SystemExit(f"gathered rows hold {got} iterations, expected {total_its / args.steps}")
     e2e_s = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
@@ -443,21 +462,34 @@ def main():
     # workloads on the device, lower, run, compute_metrics -- timed once per rank
     api = None
     if not args.no_api:
-        from paper_2508_03148_b200.api import simulate
+        from paper_2508_03148_b200.api import simulate, simulate_rows
         import copy as _copy
         simulate(_copy.deepcopy(docs[:64]), engine=eng, device_workload=True)  # warm
-        t0 = time.perf_counter()
-        bundles = simulate(_copy.deepcopy(docs), engine=eng, device_workload=True)
-        api_s = time.perf_counter() - t0
-        n_fail = sum(1 for b in bundles if not hasattr(b, "to_dict"))
-        api = {"value": iters_per_step / api_s, "unit": UNIT, "seconds": api_s,
-               "failures": n_fail,
-               "note": "simulate(docs, device_workload=True): config parsing and validation, "
-                       "device workload generation, lowering, fs_run_batch, compute_metrics"}
+        if strong and world > 1:
+            dist.barrier()
+            t0 = time.perf_counter()
+            sr = simulate_rows(_copy.deepcopy(all_docs), engine=eng, device_workload=True)
+            api_s = time.perf_counter() - t0
+            n_fail = len(sr.failed)
+            note = ("simulate_rows(all docs, device_workload=True) under torchrun: every rank "
+                    "parses, LPT-shards, simulates its shard; rows all-gathered over NCCL")
+            api_its = int(sr.rows["iterations"].sum())
+        else:
+            t0 = time.perf_counter()
+            bundles = simulate(_copy.deepcopy(docs), engine=eng, device_workload=True,
+                               expert_imbalance=False)
+            api_s = time.perf_counter() - t0
+            n_fail = sum(1 for b in bundles if not hasattr(b, "to_dict"))
+            note = ("simulate(docs, device_workload=True, expert_imbalance=False): config "
+                    "parsing and validation, device workload generation, lowering, "
+                    "fs_run_batch, compute_metrics (MetricsBundle per instance)")
+            api_its = iters_per_step
+        api = {"value": api_its / api_s, "unit": UNIT, "seconds": api_s, "failures": n_fail,
+               "note": note}
 
     # the only collective: gather every rank's fixed-size metric rows (NCCL)
     gather_ms = None
-    if world > 1:
+    if world > 1 and not strong:
         rows_t = torch.from_numpy(raw.rows.view(np.uint8).copy()).to(cdev)
         out = [torch.empty_like(rows_t) for _ in range(world)]
         torch.cuda.synchronize()
@@ -521,11 +553,12 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64+int64", "data": "synthetic",
             "config": {"workload": "C5 design-space sweep: 64 configs x "
-                                   f"{args.seeds} seeds x {args.requests} requests per GPU",
-                       "instances_per_gpu": low.n_instances, "iterations_per_step": iters_per_step * world,
+                                   f"{args.seeds} seeds x {args.requests} requests "
+                                   + ("in total, LPT-sharded over the GPUs" if strong else "per GPU"),
+                       "instances_per_gpu": low.n_instances, "iterations_per_step": int(total_its) // args.steps,
                        "parallelism": f"instances sharded over {world} GPU(s), NCCL gather of rows",
                        "l2": "flushed between steps (256 MB write, outside events)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),

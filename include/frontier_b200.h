@@ -366,7 +366,9 @@ int fs_stage(fs_engine* e,
              const fs_seed_prefix* prefixes, int32_t n_prefixes,
              const int64_t* trace_counts, int64_t n_trace_counts,
              fs_request_soa requests, int64_t n_requests);
-/* Launch the simulation + metrics kernels on `stream` (a cudaStream_t, may be 0). */
+/* Launch the simulation + metrics kernels on `stream` (a cudaStream_t, may be 0).
+ * Fails (and launches nothing) when the staged batch uses learned models and
+ * fs_set_forests replaced them after fs_stage. */
 int fs_launch_async(fs_engine* e, void* stream);
 /* Copy results of the last launch to host buffers (synchronizes the stream). */
 int fs_fetch(fs_engine* e, fs_metric_row* rows_out, fs_replica_out* replica_out,

@@ -344,6 +344,21 @@ static double pysum_result(const pysum_t* s) {
 }
 /* round(x) for a float: half-to-even, core.py:25-35 */
 static int64_t py_round(double x) { return (int64_t)llrint(x); }
+/* Python round(x, 6) for 0 <= x*1e6 < 2^52 (floatobject.c double_round): the exact
+ * product x*1e6 = hi + lo decides the integer, ties to even; n / 1e6 is the double
+ * nearest n * 10^-6. */
+static double py_round6(double x) {
+  double hi = x * 1e6;
+  double lo = fma(x, 1e6, -hi);
+  double n = rint(hi);
+  double f = hi - n;
+  double up = (f - 0.5) + lo, dn = (f + 0.5) + lo;
+  int odd = fmod(n, 2.0) != 0.0;
+  if (up > 0.0 || (up == 0.0 && odd)) n += 1.0;
+  else if (dn < 0.0 || (dn == 0.0 && odd)) n -= 1.0;
+  return n / 1e6;
+}
+double fso_round6(double x) { return py_round6(x); }
 static double py_max(double a, double b) { return (b > a) ? b : a; }
 static double py_min(double a, double b) { return (b < a) ? b : a; }
 
@@ -1033,7 +1048,7 @@ static void olog_batch(Sim* s, int bi, int64_t t_complete, int64_t seq, int64_t 
     if (b->n_moe) {
       br->moe_offset = s->log_eoff; br->n_moe = b->n_moe;
       for (int q = 0; q < b->n_moe; q++)
-        log->moe_ratio[log->moe_base[inst] + s->log_eoff + q] = b->moe[q];
+        log->moe_ratio[log->moe_base[inst] + s->log_eoff + q] = py_round6(b->moe[q]);
       s->log_eoff += b->n_moe;
     } else { br->moe_offset = -1; br->n_moe = 0; }
     log->batch_count[inst] = c + 1;

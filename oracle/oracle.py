@@ -76,11 +76,12 @@ def load():
     return lib
 
 
-def run(low: Lowered, log: LogSpec | None = None, threads: int = 1) -> RawResults:
+def run(low: Lowered, log: LogSpec | None = None, threads: int = 1,
+        log_sizes: dict | None = None) -> RawResults:
     lib = load()
     res = alloc_results(low)
     if log is not None:
-        res.log = make_log(low.n_instances, log)
+        res.log = make_log(low.n_instances, log, log_sizes)
     pr = abi.RequestOut(abi.ptr(res.first_ns), abi.ptr(res.done_ns), abi.ptr(res.done_rank))
     fset = forest_set_struct(low.forests) if low.forests is not None else None
     lib.fso_run_batch(abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas),
@@ -170,3 +171,15 @@ def generate_workload(descs):
 def pysum(xs) -> float:
     a = np.ascontiguousarray(xs, dtype=np.float64)
     return load().fso_pysum(abi.ptr(a), len(a))
+
+
+class OracleEngine:
+    """The oracle behind the Engine interface (run(lowered, log=...)) -- lets tests
+    drive the host API (simulate, make_simulation, refbind) on CPU."""
+
+    def __init__(self, threads: int = 8) -> None:
+        self.threads = threads
+        self.last_launch_count = 0
+
+    def run(self, low: Lowered, log: LogSpec | None = None, log_sizes: dict | None = None):
+        return run(low, log=log, threads=self.threads, log_sizes=log_sizes)

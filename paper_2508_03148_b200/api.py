@@ -9,15 +9,18 @@ the reference's per-point loop over `run_one` (cli.py:82-102, 197-237).
 
 from __future__ import annotations
 
+import math
 import time
 
 import numpy as np
 from dataclasses import dataclass
 
 from .config import DeploymentConfig, parse_config
+from .distributed import gather_rows, lpt_shards, merge_shards
 from .costmodel import check_model_slots_engine
+from . import abi
 from .engine import Engine, LogSpec, default_engine
-from .lower import InstanceSpec, Lowered, lower
+from .lower import InstanceSpec, Lowered, check_spec, lower
 from .metrics import InstanceResult, MetricsBundle, compute_metrics, split_results
 
 
@@ -37,12 +40,14 @@ def instance_spec(config: DeploymentConfig, requests=None) -> InstanceSpec:
     (RequestArrays) replaces the host generation when given (device_workload)."""
     attention_model, grouped_model = config.cost_model.load_models()
     check_model_slots_engine(attention_model, grouped_model)
-    return InstanceSpec(
+    spec = InstanceSpec(
         deployment=config.deployment(),
         requests=requests if requests is not None else config.request_arrays(),
         policy=config.policy,
         af=config.af if config.mode == "af" else None, routing=config.routing, seed=config.seed,
         attention_model=attention_model, grouped_gemm_model=grouped_model)
+    check_spec(spec)
+    return spec
 
 
 @dataclass
@@ -98,18 +103,134 @@ def device_request_arrays(configs: list[DeploymentConfig], engine: Engine | None
     return out
 
 
+def _metrics_or_failure(res: InstanceResult) -> MetricsBundle | Failure:
+    """compute_metrics, or the exception the reference would raise, as a Failure."""
+    if not res.ok:
+        return Failure(res.error())
+    try:
+        return compute_metrics(res)
+    except Exception as exc:  # IncompleteTrace (e.g. no requests), metrics.py:115-121
+        return Failure(exc)
+
+
+def attach_expert_imbalance(specs: list[InstanceSpec], results: list[InstanceResult],
+                            engine: Engine | None = None) -> None:
+    """Fill InstanceResult.expert_imbalance for the successful MoE instances: they are
+    simulated once more with a batch log sized exactly from the first run's counts
+    (batches = iterations, members = total_tokens, moe values = L per prefill/decode
+    batch); the values arrive from the device already as round(x, 6)."""
+    idx = [i for i, (sp, r) in enumerate(zip(specs, results))
+           if r.ok and sp.deployment.model.moe is not None]
+    if not idx:
+        return
+    eng = engine or default_engine()
+    sub = [specs[i] for i in idx]
+    rows = [results[i].row for i in idx]
+    nb = [int(r["iterations"]) for r in rows]
+    nm = [int(r["total_tokens"]) for r in rows]
+    ne = [(int(r["prefill_batches"]) + int(r["decode_batches"])) * sp.deployment.model.num_layers
+          for r, sp in zip(rows, sub)]
+    spec = LogSpec(batch_cap=max(nb), member_cap=max(nm), moe_cap=max(max(ne), 1))
+    raw = eng.run(lower(sub), log=spec, log_sizes={"batch": nb, "member": nm, "moe": ne})
+    for j, i in enumerate(idx):
+        if raw.log.truncated[j]:
+            raise RuntimeError(f"instance {i}: moe-ratio log truncated on the re-run")
+        results[i].expert_imbalance = raw.log.moe_imbalance(j)
+
+
+# ---- multi-GPU sharding (SURVEY 8(e)) ----------------------------------------------------
+
+def process_group(distributed: bool | None):
+    """torch.distributed when it should shard (initialised, world > 1), else None."""
+    if distributed is False:
+        return None
+    try:
+        import torch.distributed as dist
+    except Exception:  # pragma: no cover
+        dist = None
+    if dist is not None and dist.is_available() and dist.is_initialized() \
+            and dist.get_world_size() > 1:
+        return dist
+    if distributed:
+        raise RuntimeError("distributed=True needs an initialised torch.distributed group")
+    return None
+
+
+def config_cost(config: DeploymentConfig) -> int:
+    """Host estimate of an instance's device time for LPT sharding: iterations are
+    ~ output tokens, each costs ~ L layers, MoE layers route T x E keys
+    (lower._estimate_cost's shape, from the config alone -- no workload drawn)."""
+    m = config.model
+    wl = config.workload
+    if wl is None:
+        out_tokens = 256 * 64
+    else:
+        o = wl.output_len
+        mean = (o.value if o.kind == "fixed" else (o.lo + o.hi) / 2 if o.kind == "uniform"
+                else min(max(math.exp(o.mu + o.sigma * o.sigma / 2), o.lo), o.hi))
+        out_tokens = wl.num_requests * (mean + 1)
+    work = out_tokens * m.num_layers
+    if m.moe is not None:
+        work *= 1 + m.moe.num_experts / 4
+    return int(work)
+
+
+def _parse(c, base_dir: str):
+    if isinstance(c, (DeploymentConfig, Failure)):
+        return c
+    try:
+        return parse_config(c, base_dir=base_dir)
+    except Exception as exc:  # config-time failures (cli.py:229-233)
+        return Failure(exc)
+
+
+def shard_plan(configs: list, world: int, base_dir: str = "."):
+    """(parsed configs or Failures, LPT shards over ranks): same on every rank."""
+    parsed = [_parse(c, base_dir) for c in configs]
+    costs = [config_cost(p) if isinstance(p, DeploymentConfig) else 0 for p in parsed]
+    return parsed, lpt_shards(costs, world)
+
+
+def _simulate_sharded(dist, configs, engine, base_dir, device_workload, expert_imbalance):
+    rank, world = dist.get_rank(), dist.get_world_size()
+    parsed, shards = shard_plan(configs, world, base_dir)
+    mine = shards[rank]
+    local = simulate([parsed[i] for i in mine], engine=engine, base_dir=base_dir,
+                     device_workload=device_workload, expert_imbalance=expert_imbalance,
+                     distributed=False)
+    gathered: list = [None] * world
+    dist.all_gather_object(gathered, local)  # bundles carry per-request dicts: pickled
+    out: list = [None] * len(configs)
+    for idx, res in zip(shards, gathered):
+        for i, r in zip(idx, res):
+            out[i] = r
+    return out
+
+
 def simulate(configs: list, engine: Engine | None = None, base_dir: str = ".",
-             device_workload: bool = False) -> list[MetricsBundle | Failure]:
+             device_workload: bool = False, expert_imbalance: bool = True,
+             distributed: bool | None = None) -> list[MetricsBundle | Failure]:
     """Simulate every config on the GPU; per-instance errors become Failure entries.
-    device_workload: draw the synthetic request streams on the device too."""
+    device_workload: draw the synthetic request streams on the device too.
+    expert_imbalance: fill MetricsBundle.expert_imbalance for MoE configs (a second
+    device pass over them, see attach_expert_imbalance); False leaves it None --
+    the sweep's CSV and frontier do not use it.
+    distributed: with torch.distributed initialised (world > 1; None = auto), every
+    rank simulates its LPT shard on its own GPU and the results are all-gathered,
+    so each rank returns the full list in input order."""
+    dist = process_group(distributed)
+    if dist is not None:
+        return _simulate_sharded(dist, configs, engine, base_dir, device_workload,
+                                 expert_imbalance)
     out: list[MetricsBundle | Failure | None] = [None] * len(configs)
     specs, where = [], []
     parsed: list = [None] * len(configs)
     for i, c in enumerate(configs):
-        try:
-            parsed[i] = c if isinstance(c, DeploymentConfig) else parse_config(c, base_dir=base_dir)
-        except Exception as exc:  # config-time failures (cli.py:229-233)
-            out[i] = Failure(exc)
+        p = c if isinstance(c, Failure) else _parse(c, base_dir)
+        if isinstance(p, Failure):
+            out[i] = p
+        else:
+            parsed[i] = p
     pre: list = [None] * len(configs)
     if device_workload:
         ok = [i for i in range(len(configs)) if parsed[i] is not None]
@@ -127,8 +248,10 @@ def simulate(configs: list, engine: Engine | None = None, base_dir: str = ".",
             out[i] = Failure(exc)
     if specs:
         run = run_specs(specs, engine)
+        if expert_imbalance:
+            attach_expert_imbalance(specs, run.results, engine)
         for i, res in zip(where, run.results):
-            out[i] = compute_metrics(res) if res.ok else Failure(res.error())
+            out[i] = _metrics_or_failure(res)
     return out
 
 
@@ -143,3 +266,101 @@ def run_one(config: DeploymentConfig, engine: Engine | None = None) -> dict:
     trace = sim.run()
     return {"config": config, "trace": trace, "metrics": compute_metrics(trace, spec.deployment),
             "config_hash": config.config_hash()}
+
+
+# ---- rows-only path: the sweep driver's fixed-size metric rows --------------------------
+
+@dataclass
+class SweepRows:
+    """Metric rows of a batch of configs, in input order: `rows` (fs_metric_row) for
+    every instance that reached the device, `failed` = {index: "Type: msg"} for the
+    others (their rows are zero), `config_hash` and `total_gpus` per instance (None
+    if it never reached the device)."""
+
+    rows: np.ndarray
+    failed: dict[int, str]
+    config_hash: list[str | None]
+    total_gpus: list[int | None]
+
+    def bundle(self, i: int) -> MetricsBundle | None:
+        return None if i in self.failed else bundle_from_row(self.rows[i], self.total_gpus[i])
+
+
+def simulate_rows(configs: list, engine: Engine | None = None, base_dir: str = ".",
+                  device_workload: bool = False, distributed: bool | None = None) -> SweepRows:
+    """simulate() reduced to the fixed-size metric rows, which is all a sweep's CSV and
+    frontier read. Multi-GPU: LPT shards per rank, one all-gather of the rows over
+    the process group (NCCL on the B200 box) plus the failure texts."""
+    dist = process_group(distributed)
+    world, rank = (dist.get_world_size(), dist.get_rank()) if dist is not None else (1, 0)
+    parsed, shards = shard_plan(configs, world, base_dir)
+    mine = shards[rank]
+    specs, where, failed, hashes = [], [], {}, {}
+    pre: dict[int, object] = {}
+    if device_workload:
+        ok = [i for i in mine if isinstance(parsed[i], DeploymentConfig)]
+        for i, r in zip(ok, device_request_arrays([parsed[i] for i in ok], engine)):
+            pre[i] = r
+    for i in mine:
+        p = parsed[i]
+        try:
+            if isinstance(p, Failure):
+                raise p.exception
+            if isinstance(pre.get(i), Exception):
+                raise pre[i]
+            sp = instance_spec(p, requests=pre.get(i))
+            specs.append(sp)
+            where.append(i)
+            hashes[i] = (p.config_hash(), sp.deployment.total_gpus)
+        except Exception as exc:
+            failed[i] = f"{type(exc).__name__}: {exc}"
+    local = np.zeros(len(mine), dtype=abi.METRIC_ROW)
+    if specs:
+        run = run_specs(specs, engine)
+        pos = {i: j for j, i in enumerate(mine)}
+        for i, res in zip(where, run.results):
+            local[pos[i]] = res.row
+            if not res.ok:
+                failed[i] = f"{type(res.error()).__name__}: {res.error()}"
+            elif len(res.request_ids) == 0:
+                failed[i] = "IncompleteTrace: trace contains no requests"
+    if dist is None:
+        rows = merge_shards(shards, [local], len(configs))
+        meta = [(failed, hashes)]
+    else:
+        rows = merge_shards(shards, gather_rows(local, world, _row_device()), len(configs))
+        meta: list = [None] * world
+        dist.all_gather_object(meta, (failed, hashes))
+    all_failed, all_hash = {}, {}
+    for f, h in meta:
+        all_failed.update(f)
+        all_hash.update(h)
+    n = len(configs)
+    return SweepRows(rows, dict(sorted(all_failed.items())),
+                     [all_hash[i][0] if i in all_hash else None for i in range(n)],
+                     [all_hash[i][1] if i in all_hash else None for i in range(n)])
+
+
+def _row_device():
+    """Where gather_rows stages its buffers: this rank's GPU under NCCL, host for gloo."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return None
+
+
+def bundle_from_row(row: np.void, total_gpus: int) -> MetricsBundle:
+    """The aggregate part of a MetricsBundle from its metric row (what summary_csv_row
+    and pareto_frontier read); per_request / busy / expert_imbalance are not in a row."""
+    from .metrics import _agg, _nan_to_none
+    thr = float(row["throughput_tokens_per_s_per_gpu"])
+    return MetricsBundle(
+        per_request={}, ttft=_agg(row["ttft"]), tpot=_agg(row["tpot"]), e2e=_agg(row["e2e"]),
+        total_tokens=int(row["total_tokens"]), makespan_s=float(row["makespan_s"]),
+        total_gpus=total_gpus, throughput_tokens_per_s_per_gpu=thr, busy_fraction={},
+        bubble_fraction=_nan_to_none(float(row["bubble_fraction"])), expert_imbalance=None,
+        workload_summary={"batch_size": int(row["n_requests"]),
+                          "avg_input_tokens": float(row["avg_input_tokens"]),
+                          "avg_output_tokens": float(row["avg_output_tokens"]),
+                          "throughput_tokens_per_s_per_gpu": thr})

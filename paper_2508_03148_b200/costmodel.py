@@ -59,6 +59,19 @@ def load_model_file(path: str) -> LearnedModel:
     opener = gzip.open if path.endswith(".gz") else open
     with opener(path, "rt", encoding="utf-8") as fh:
         doc = json.load(fh)
+    return model_from_document(doc, path)
+
+
+def as_learned_model(model) -> LearnedModel | None:
+    """A LearnedModel from one of ours or from the reference's LearnedOperatorModel
+    (its portable document, costmodel/model.py:140-152)."""
+    if model is None or isinstance(model, LearnedModel):
+        return model
+    return model_from_document(model.to_document(), f"<{model.operator} model>")
+
+
+def model_from_document(doc: dict, path: str = "<document>") -> LearnedModel:
+    """Pack a model document (load_model_file's checks, model.py:169-182)."""
     if doc.get("format") != MODEL_FILE_FORMAT:
         raise ModelFileError(f"{path}: not a {MODEL_FILE_FORMAT} file")
     if doc.get("hash") != _document_hash(doc):

@@ -61,6 +61,9 @@ struct fs_engine {
   // learned models (persist across stages)
   DevBuf f_descs, f_roots, f_right, f_value, f_leaf;  // f_value: packed NodeP array
   fs::ForestView fv{};
+  int64_t forest_gen = 0;         // bumped by every fs_set_forests
+  int64_t staged_forest_gen = -1; // forest_gen the staged batch's indices refer to
+  bool staged_uses_forests = false;
   bool learned = false;  // staged batch uses the learned simulation variant
   int variant = 0;       // fs::SimVariant of the staged batch
   int n_moe = 0;         // MoE instances of the staged batch (first in the order)
@@ -273,6 +276,8 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   P.log_enabled = 0;
   // routing job board: one slot per resident warp of the persistent grid
   e->learned = false;
+  e->staged_uses_forests = false;
+  e->staged_forest_gen = e->forest_gen;
   for (int i = 0; i < n_instances; i++) {
     const int32_t fsel[2] = {descs[i].attn_forest, descs[i].gg_forest};
     for (int32_t f : fsel) {
@@ -281,6 +286,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
         return 13;
       }
       if (f != -1) e->learned = true;
+      if (f >= 0) e->staged_uses_forests = true;
     }
     // dirichlet_skew routing is compiled into the extended (learned) kernel variant only
     if (descs[i].has_moe && descs[i].routing_policy == FS_ROUTE_DIRICHLET) e->learned = true;
@@ -334,6 +340,12 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
 
 int fs_launch_async(fs_engine* e, void* stream) {
   if (!e || !e->staged) return 1;
+  if (e->staged_uses_forests && e->staged_forest_gen != e->forest_gen) {
+    // the staged instances' forest indices refer to a forest set that has been
+    // replaced since fs_stage: running them would silently use other models
+    e->err = "fs_set_forests was called after fs_stage; stage the batch again";
+    return 14;
+  }
   cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
   FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
   FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
@@ -677,6 +689,7 @@ int fs_set_forests(fs_engine* e, fs_forest_set f) {
   e->fv.right = e->f_right.as<int32_t>();
   e->fv.leaf_by_rank = e->f_leaf.as<double>();
   e->params.fv = e->fv;
+  e->forest_gen++;
   return 0;
 }
 

@@ -19,6 +19,22 @@ __device__ __forceinline__ double py_max(double a, double b) { return b > a ? b 
 __device__ __forceinline__ double py_min(double a, double b) { return b < a ? b : a; }
 // round(x) -> int, half to even (core.py:25-35)
 __device__ __forceinline__ int64_t py_round(double x) { return __double2ll_rn(x); }
+// Python's round(x, 6) (floatobject.c double_round: correctly rounded to 6
+// decimals, ties to even on the exact binary value), for 0 <= x*1e6 < 2^52 --
+// the moe_imbalance report format (base.py:247-252; ratios are >= 1). The exact
+// product x*1e6 = hi + lo (FMA residual) decides the integer n; n / 1e6 is then
+// the double nearest n * 10^-6, which is what strtod of the rounded decimal gives.
+__device__ __forceinline__ double py_round6(double x) {
+  const double hi = __dmul_rn(x, 1e6);
+  const double lo = __fma_rn(x, 1e6, -hi);
+  double n = rint(hi);
+  const double f = __dsub_rn(hi, n);  // exact, |f| <= 0.5
+  const double up = __dadd_rn(__dsub_rn(f, 0.5), lo), dn = __dadd_rn(__dadd_rn(f, 0.5), lo);
+  const bool odd = fmod(n, 2.0) != 0.0;
+  if (up > 0.0 || (up == 0.0 && odd)) n = __dadd_rn(n, 1.0);
+  else if (dn < 0.0 || (dn == 0.0 && odd)) n = __dsub_rn(n, 1.0);
+  return __ddiv_rn(n, 1e6);
+}
 __device__ __forceinline__ double i2d(int64_t v) { return __ll2double_rn(v); }
 
 // CPython 3.12 builtin sum() of floats from int 0: first item exact, the rest

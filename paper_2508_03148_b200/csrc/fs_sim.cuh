@@ -890,8 +890,8 @@ __device__ __noinline__ int learned_moe_layer_warp(const EngineParams& P, Inst& 
 #define FFN_DENSE_US(c, n) dense_ffn_us(d, (c), (n))
 #endif
 
-// Duration in us (same on all lanes). moe_out (global) receives per-layer raw
-// moe_imbalance ratios when non-null.
+// Duration in us (same on all lanes). moe_out (global) receives the per-layer
+// moe_imbalance values round(expert / mean(per_rank), 6) when non-null.
 __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
                                 const BatchShape& b, int64_t step, WarpSmem* sm,
                                 double* moe_out) {
@@ -966,7 +966,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
           if (st != FS_OK) { fail(I, st, l); return 0.0; }
         }
         __syncwarp();
-        if (moe_out && I.lane == 0) moe_out[l] = ratio;
+        if (moe_out && I.lane == 0) moe_out[l] = py_round6(ratio);
         double tot = qkv + att;
         tot = tot + out;
         tot = tot + coll;

@@ -116,22 +116,23 @@ class RawLog:
     c_struct: abi.LogC
     events: np.ndarray | None = None
     event_count: np.ndarray | None = None
+    bases: dict | None = None
 
     def instance_batches(self, i: int) -> list[dict]:
         """Batch records of instance i in BATCH_COMPLETE dispatch order (t_complete, seq);
         the engine records them when they start. `index` = position in the raw log."""
-        s = self.spec
         n = int(self.batch_count[i])
-        raw = self.batches[i * s.batch_cap: i * s.batch_cap + n]
+        bb, mb, eb = self.bases["batch"][i], self.bases["member"][i], self.bases["moe"][i]
+        raw = self.batches[bb: bb + n]
         order = np.lexsort((raw["seq"], raw["t_complete"])) if n else []
         out = []
         for j in order:
             b = raw[j]
             mo = int(b["member_offset"])
-            mem = self.members[i * s.member_cap + mo: i * s.member_cap + mo + int(b["n_members"])]
+            mem = self.members[mb + mo: mb + mo + int(b["n_members"])]
             moe = None
             if b["n_moe"] > 0:
-                eo = i * s.moe_cap + int(b["moe_offset"])
+                eo = eb + int(b["moe_offset"])
                 moe = self.moe[eo: eo + int(b["n_moe"])].tolist()
             out.append({"replica": int(b["replica"]), "phase": abi.PHASES[int(b["phase"])],
                         "t_complete": int(b["t_complete"]), "duration_ns": int(b["duration_ns"]),
@@ -146,14 +147,31 @@ class RawLog:
         n = int(self.event_count[i])
         if n > cap:
             raise RuntimeError(f"event log of instance {i} truncated ({n} events, cap {cap})")
-        return self.events[i * cap: i * cap + n].copy()
+        b = self.bases["event"][i]
+        return self.events[b: b + n].copy()
+
+    def moe_imbalance(self, i: int) -> list[float]:
+        """expert_imbalance of instance i (metrics.py:105-109): the per-layer values of
+        its prefill/decode batches in BATCH_COMPLETE order (already round(x, 6))."""
+        n = int(self.batch_count[i])
+        if n == 0:
+            return []
+        bb, eb = self.bases["batch"][i], self.bases["moe"][i]
+        raw = self.batches[bb: bb + n]
+        raw = raw[np.lexsort((raw["seq"], raw["t_complete"]))]
+        raw = raw[raw["n_moe"] > 0]
+        if len(raw) == 0:
+            return []
+        L = int(raw["n_moe"][0])
+        idx = eb + raw["moe_offset"].astype(np.int64)[:, None] + np.arange(L)[None, :]
+        return self.moe[idx.ravel()].tolist()
 
     def instance_routes(self, i: int) -> list[dict]:
-        s = self.spec
         out = []
+        rb, cb = self.bases["route"][i], self.bases["counts"][i]
         for j in range(int(self.route_count[i])):
-            r = self.routes[i * s.route_cap + j]
-            co = i * s.counts_cap + int(r["counts_offset"])
+            r = self.routes[rb + j]
+            co = cb + int(r["counts_offset"])
             out.append({"replica": int(r["replica"]), "micro_batch": int(r["micro_batch"]),
                         "step": int(r["step"]), "layer": int(r["layer"]),
                         "tokens": int(r["tokens"]),
@@ -161,25 +179,38 @@ class RawLog:
         return out
 
 
-def make_log(n_instances: int, spec: LogSpec) -> RawLog:
-    def bases(cap):
-        return np.arange(n_instances, dtype=np.int64) * cap
+_LOG_FIELDS = ("batch", "member", "moe", "route", "counts", "event")
+
+
+def make_log(n_instances: int, spec: LogSpec, sizes: dict | None = None) -> RawLog:
+    """Log buffers: instance i owns [base_i, base_i + cap) of each array. `sizes`
+    (field -> per-instance int array) packs regions of exactly those sizes instead
+    of `cap` each -- for a re-run whose record counts are known, since a run
+    never writes more records than it produces (the caps stay the maxima)."""
+    sizes = sizes or {}
+    bases, total = {}, {}
+    for f in _LOG_FIELDS:
+        cap = getattr(spec, f + "_cap")
+        sz = np.asarray(sizes[f], dtype=np.int64) if f in sizes else np.full(n_instances, cap, np.int64)
+        bases[f] = np.concatenate([[0], np.cumsum(sz)[:-1]]).astype(np.int64) if n_instances \
+            else np.zeros(0, np.int64)
+        total[f] = int(sz.sum()) if cap else 0
     log = RawLog(
         spec=spec,
-        batches=np.zeros(max(1, n_instances * spec.batch_cap), dtype=abi.BATCH_REC),
-        members=np.zeros(max(1, n_instances * spec.member_cap), dtype=np.int32),
-        moe=np.zeros(max(1, n_instances * spec.moe_cap), dtype=np.float64),
-        routes=np.zeros(max(1, n_instances * spec.route_cap), dtype=abi.ROUTE_REC),
-        counts=np.zeros(max(1, n_instances * spec.counts_cap), dtype=np.int32),
+        batches=np.zeros(max(1, total["batch"]), dtype=abi.BATCH_REC),
+        members=np.zeros(max(1, total["member"]), dtype=np.int32),
+        moe=np.zeros(max(1, total["moe"]), dtype=np.float64),
+        routes=np.zeros(max(1, total["route"]), dtype=abi.ROUTE_REC),
+        counts=np.zeros(max(1, total["counts"]), dtype=np.int32),
         batch_count=np.zeros(n_instances, dtype=np.int32),
         route_count=np.zeros(n_instances, dtype=np.int32),
         truncated=np.zeros(n_instances, dtype=np.int32),
         c_struct=abi.LogC(),
-        events=np.zeros(max(1, n_instances * spec.event_cap), dtype=abi.EVENT_REC),
+        events=np.zeros(max(1, total["event"]), dtype=abi.EVENT_REC),
         event_count=np.zeros(n_instances, dtype=np.int64))
+    log.bases = bases
     c = log.c_struct
-    log._keep = [bases(spec.batch_cap), bases(spec.member_cap), bases(spec.moe_cap),
-                 bases(spec.route_cap), bases(spec.counts_cap), bases(spec.event_cap)]
+    log._keep = [bases[f] for f in _LOG_FIELDS]
     c.event_base = abi.ptr(log._keep[5])
     c.event_cap = spec.event_cap
     c.events = abi.ptr(log.events) if spec.event_cap else None
@@ -267,11 +298,12 @@ class Engine:
         self._check(self.lib.fs_set_forests(self.h, forest_set_struct(forests)), "fs_set_forests")
         self._forests = forests
 
-    def run(self, low: Lowered, log: LogSpec | None = None) -> RawResults:
+    def run(self, low: Lowered, log: LogSpec | None = None,
+            log_sizes: dict | None = None) -> RawResults:
         self.set_forests(low.forests)
         res = alloc_results(low)
         if log is not None:
-            res.log = make_log(low.n_instances, log)
+            res.log = make_log(low.n_instances, log, log_sizes)
         pr = abi.RequestOut(abi.ptr(res.first_ns), abi.ptr(res.done_ns), abi.ptr(res.done_rank))
         rc = self.lib.fs_run_batch(
             self.h, abi.ptr(low.descs), low.n_instances, abi.ptr(low.replicas), len(low.replicas),

@@ -127,6 +127,38 @@ class Lowered:
         return len(self.arrival)
 
 
+def check_spec(sp: InstanceSpec) -> None:
+    """The per-instance checks the reference makes inside make_simulation
+    (base.py:71-111, af.py:381-392, cluster.py:108-118) plus the engine's
+    capacity limits. simulate() runs this per point, so a bad point becomes a
+    Failure row (cli.py:229-233) and lower() cannot raise for the others."""
+    dep, model = sp.deployment, sp.deployment.model
+    sp.policy.validate()
+    if len(set(sp.requests.ids)) != len(sp.requests.ids):
+        raise SimulationError("duplicate request id")
+    layout = replica_layout(dep)
+    if not layout:
+        raise SimulationError(f"{dep.mode} deployment has no serving replicas")
+    if len(layout) > abi.MAX_REPLICAS:
+        raise EngineCapacityError(f"{len(layout)} replicas exceed {abi.MAX_REPLICAS}")
+    if model.moe is not None and model.moe.num_experts > abi.MAX_EXPERTS:
+        raise EngineCapacityError(f"{model.moe.num_experts} experts exceed {abi.MAX_EXPERTS}")
+    for ri in layout:
+        _prefix(f"{sp.seed}:{ri.key}:mb")  # router-seed prefix length
+    if dep.mode == "af":
+        (sp.af or AfPipelineConfig()).validate()
+        attn = dep.clusters_with_role("attention")
+        ffn = dep.clusters_with_role("ffn")
+        if len(attn) != 1 or len(ffn) != 1:
+            raise ValueError("af mode takes exactly one attention and one ffn cluster")
+        if attn[0].num_replicas != 1 or ffn[0].num_replicas != 1:
+            raise ValueError("af mode models a single pipeline: num_replicas must be 1")
+    for m, schema in ((sp.attention_model, "attention_v1"),
+                      (sp.grouped_gemm_model, "grouped_gemm_v1")):
+        if m is not None and m.schema == schema and m.n_trees > abi.MAX_FOREST_TREES:
+            raise EngineCapacityError(f"{m.path}: {m.n_trees} trees exceed {abi.MAX_FOREST_TREES}")
+
+
 def lower(specs: list[InstanceSpec]) -> Lowered:
     n = len(specs)
     descs = np.zeros(n, dtype=abi.INSTANCE_DESC)
@@ -139,14 +171,8 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
     forests = ForestSet()
     for i, sp in enumerate(specs):
         dep, model, pol = sp.deployment, sp.deployment.model, sp.policy
-        pol.validate()
-        if len(set(sp.requests.ids)) != len(sp.requests.ids):
-            raise SimulationError("duplicate request id")
+        check_spec(sp)
         layout = replica_layout(dep)
-        if not layout:
-            raise SimulationError(f"{dep.mode} deployment has no serving replicas")
-        if len(layout) > abi.MAX_REPLICAS:
-            raise EngineCapacityError(f"{len(layout)} replicas exceed {abi.MAX_REPLICAS}")
         d = descs[i]
         d["mode"] = abi.MODE[dep.mode]
         d["n_requests"] = len(sp.requests)

@@ -34,7 +34,7 @@ class MetricsBundle:
     throughput_tokens_per_s_per_gpu: float
     busy_fraction: dict[str, float]
     bubble_fraction: float | None
-    expert_imbalance: list[float]
+    expert_imbalance: list[float] | None
     workload_summary: dict[str, float]
 
     def to_dict(self) -> dict:
@@ -78,6 +78,7 @@ class InstanceResult:
     kv_bytes_per_token: int = 0
     af_micro_batches: int = 0
     event_log: np.ndarray | None = None      # fs_event_rec by seq (trace runs only)
+    expert_imbalance: list[float] | None = None  # from a moe-ratio log (api.simulate)
 
     def trace(self):
         """The reference's EventTrace of this run (needs a run with an event log)."""
@@ -189,11 +190,18 @@ def compute_metrics(result, deployment=None) -> MetricsBundle:
         for j, name in enumerate(abi.AF_RESOURCES):
             busy[name] = float(row["af_busy_fraction"][j])
     busy = dict(sorted(busy.items()))
-    imbalance: list[float] = []
-    if result.batches is not None:
+    # expert_imbalance (metrics.py:105-109): [] without MoE; for MoE runs it needs a
+    # batch log (run_one / make_simulation record one; simulate() re-runs the MoE
+    # instances with one unless expert_imbalance=False, which leaves None here)
+    imbalance: list[float] | None = []
+    if result.expert_imbalance is not None:
+        imbalance = result.expert_imbalance
+    elif result.batches is not None:
         for b in result.batches:
             if b["moe_ratio"] is not None:
                 imbalance.extend(round(x, 6) for x in b["moe_ratio"])
+    elif result.has_moe:
+        imbalance = None
     thr = float(row["throughput_tokens_per_s_per_gpu"])
     return MetricsBundle(
         per_request=per_request,

@@ -13,7 +13,7 @@ timestamps), as the reference's handlers leave them.
 from __future__ import annotations
 
 from .cluster import SchedulerPolicy
-from .costmodel import check_model_slots_engine
+from .costmodel import as_learned_model, check_model_slots_engine
 from .engine import Engine, LogSpec, default_engine
 from .errors import RequestCannotFit, SimulationError  # noqa: F401  (re-exported)
 from .lower import InstanceSpec, lower
@@ -68,11 +68,18 @@ class Simulation:
         policy.validate()
         if mode == "af":
             (af or AfPipelineConfig()).validate()
+        attention_model = as_learned_model(attention_model)
+        grouped_gemm_model = as_learned_model(grouped_gemm_model)
         check_model_slots_engine(attention_model, grouped_gemm_model)
         self.mode = mode
         self.deployment = deployment
         self.requests = list(requests)
-        self.request_arrays: RequestArrays = arrays_from_requests(self.requests)
+        # The engine consumes arrivals in time order; equal times keep list order,
+        # which is the reference's dispatch order (seq = list index, base.py:167-177).
+        self._order = sorted(range(len(self.requests)),
+                             key=lambda i: self.requests[i].arrival_time)
+        self.request_arrays: RequestArrays = arrays_from_requests(
+            [self.requests[i] for i in self._order])
         self.spec = InstanceSpec(
             deployment=deployment, requests=self.request_arrays, policy=policy,
             af=af if mode == "af" else None, routing=routing or RoutingPolicySpec(), seed=seed,
@@ -91,10 +98,13 @@ class Simulation:
         self.result = res
         self._update_requests(res)
         res.raise_for_status()
-        return res.trace()
+        trace = res.trace()
+        if self._order != list(range(len(self._order))):
+            trace.remap_arrival_seq(self._order)
+        return trace
 
     def _update_requests(self, res: InstanceResult) -> None:
-        for i, req in enumerate(self.requests):
+        for i, req in enumerate(self.requests[j] for j in self._order):
             done = int(res.done_ns[i])
             if done >= 0:
                 req.tokens_emitted = req.output_tokens

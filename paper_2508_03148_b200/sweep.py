@@ -7,13 +7,16 @@ mirrored the master seed follows it), point failures become
 `failed: {Type}: {msg}` rows, and the Pareto frontier (throughput up, p90 TPOT
 down) is written next to `sweep.csv`. Differences:
 
-* all points are simulated in ONE batched engine call (`api.simulate`), not a
-  thread pool of per-point Python runs (which the GIL serialises, SURVEY §0.8);
+* all points are simulated in ONE batched engine call (`api.simulate_rows`), not
+  a thread pool of per-point Python runs (which the GIL serialises, SURVEY §0.8);
+  the CSV and frontier need only each point's fixed-size metric row;
 * dotted keys may index lists: `clusters.0.parallelism.tp` addresses the first
   cluster (the reference replaces the list with a dict and the point fails to
-  parse, SURVEY §0.7); `clusters.1.num_replicas` etc.;
-* with torch.distributed initialised, points are LPT-sharded across ranks and
-  the metric rows all-gathered (`distributed.py`).
+  parse); `clusters.1.num_replicas` etc.; an override that cannot
+  be applied fails its point only;
+* with torch.distributed initialised (world > 1, e.g. under torchrun), points are
+  LPT-sharded across ranks by `api.config_cost`, each rank simulates its shard on
+  its own GPU, the metric rows are all-gathered (NCCL) and rank 0 writes the files.
 """
 
 from __future__ import annotations
@@ -26,9 +29,9 @@ import json
 import os
 import tempfile
 
-from .api import Failure, simulate
+from .api import Failure, process_group, simulate_rows
 from .config import DeploymentConfig, ParseError, load_config
-from .metrics import SUMMARY_CSV_HEADER, MetricsBundle, pareto_frontier, summary_csv_row
+from .metrics import SUMMARY_CSV_HEADER, pareto_frontier, summary_csv_row
 
 
 def grid_points(grid: dict[str, list]) -> list[dict]:
@@ -72,10 +75,16 @@ def point_seed(master_seed: int, overrides: dict) -> int:
     return int.from_bytes(digest[:4], "big")
 
 
-def point_documents(document: dict, points: list[dict], master_seed: int) -> list[dict]:
-    docs = []
+def point_documents(document: dict, points: list[dict], master_seed: int) -> list:
+    """One config document per point, or a Failure for a point whose overrides
+    cannot be applied (the reference records it as a failed row)."""
+    docs: list = []
     for ov in points:
-        d = apply_overrides(document, ov)
+        try:
+            d = apply_overrides(document, ov)
+        except Exception as exc:
+            docs.append(Failure(exc))
+            continue
         d["seed"] = point_seed(master_seed, ov)
         wl = d.get("workload", {})
         if wl.get("seed") == master_seed:
@@ -99,30 +108,29 @@ def _atomic_write(path: str, data: bytes) -> None:
 
 
 def run_sweep(config: DeploymentConfig, grid: dict, out_dir: str, base_dir: str = ".",
-              engine=None) -> dict:
-    """Simulate every grid point; write sweep.csv and frontier.json to out_dir."""
+              engine=None, distributed: bool | None = None) -> dict:
+    """Simulate every grid point; write sweep.csv and frontier.json to out_dir
+    (rank 0 only when sharded over ranks)."""
     document = config.to_document()
     points = grid_points(grid)
     docs = point_documents(document, points, config.seed)
-    results = simulate(docs, engine=engine, base_dir=base_dir)
-    hashes = []
-    for d, r in zip(docs, results):
-        if isinstance(r, MetricsBundle):
-            from .config import parse_config
-            hashes.append(parse_config(copy.deepcopy(d), base_dir=base_dir).config_hash())
-        else:
-            hashes.append(None)
+    sr = simulate_rows(docs, engine=engine, base_dir=base_dir, distributed=distributed)
     buf = io.StringIO()
     w = csv.writer(buf)
     w.writerow(["point", "overrides", "status"] + SUMMARY_CSV_HEADER)
     ok = []
-    for idx, (ov, r, h) in enumerate(zip(points, results, hashes)):
+    for idx, ov in enumerate(points):
         ov_json = json.dumps(ov, sort_keys=True)
-        if isinstance(r, Failure):
-            w.writerow([idx, ov_json, r.status] + [""] * len(SUMMARY_CSV_HEADER))
+        if idx in sr.failed:
+            w.writerow([idx, ov_json, f"failed: {sr.failed[idx]}"] + [""] * len(SUMMARY_CSV_HEADER))
         else:
-            w.writerow([idx, ov_json, "ok"] + summary_csv_row(r, h))
-            ok.append((idx, r))
+            b = sr.bundle(idx)
+            w.writerow([idx, ov_json, "ok"] + summary_csv_row(b, sr.config_hash[idx]))
+            ok.append((idx, b))
+    dist = process_group(distributed)
+    if dist is not None and dist.get_rank() != 0:
+        front = pareto_frontier(ok)
+        return {"points": len(points), "ok": len(ok), "frontier": len(front)}
     _atomic_write(os.path.join(out_dir, "sweep.csv"), buf.getvalue().encode("utf-8"))
     front = pareto_frontier(ok)
     front_doc = [{"point": idx, "overrides": points[idx],

@@ -101,6 +101,13 @@ class EventTrace:
         self._records: list[SimEvent] | None = None
         self._lines: list[str] | None = None
 
+    def remap_arrival_seq(self, order: list[int]) -> None:
+        """Arrivals were simulated in time order; their seq is the caller's list
+        index (base.py:167-177): order[j] is the list index of simulated request j."""
+        arr = self._ev["kind"] == 0
+        self._ev["seq"][arr] = np.asarray(order, dtype=np.int64)[self._ev["a"][arr]]
+        self._records = self._lines = None
+
     # -- reference API -----------------------------------------------------------------
     def __len__(self) -> int:
         return len(self._ev)

@@ -12,7 +12,7 @@ import sys
 def main(rep, top=25, kernel=None):
     cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
     if kernel:
-        cmd += ["-k", f"regex:{kernel}"]
+        cmd += ["--kernel-name-base", "demangled", "-k", f"regex:{kernel}"]
     txt = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
     agg, cur_file, cur_line, cur_src, hdr = {}, None, None, "", None
     for row in csv.reader(io.StringIO(txt)):
