@@ -311,7 +311,9 @@ typedef struct {
 } fs_route_rec;               /* 32 bytes */
 
 typedef struct {
-  /* per-instance capacities and bases (arrays of n_instances) */
+  /* per-instance capacities and bases (arrays of n_instances). Instance i writes
+     at most `cap` records from base[i]; each host array must hold
+     max_i(base[i] + cap) records (that many are copied back). */
   const int64_t* batch_base;  int32_t batch_cap;
   const int64_t* member_base; int32_t member_cap;
   const int64_t* moe_base;    int32_t moe_cap;
@@ -447,6 +449,38 @@ int fs_generate_workload(fs_engine* e, const fs_workload_desc* w, int32_t n,
 int fs_router_seeds(fs_engine* e, const fs_seed_prefix* prefixes, const int32_t* prefix_idx,
                     const int32_t* micro_batch, const int64_t* steps, const int32_t* layers,
                     int32_t n, uint32_t* seeds_out);
+
+/* ---- diagnostics: the pure functions the simulator composes ----------------
+ * fs_eval evaluates one of them elementwise on the device through the same
+ * device functions sim_kernel calls, for parity tests against the reference's
+ * golden vectors (tests/test_eval.py). Records of `in_stride` doubles in,
+ * `out_stride` doubles out; integers as exact doubles; status per record.
+ * Replaces nothing in the reference (its pure functions are Python calls):
+ *   FS_EVAL_EXP/LOG/LOG1P   [x] -> [y]        libm as numpy's distributions.c
+ *   FS_EVAL_POW             [x, y] -> [z]     calls it (glibc 2.39, fs_glibm.h)
+ *   FS_EVAL_LINEAR          [m, n, k, peak_flops, mem_bw, overhead_us, dtype]
+ *                           -> [us]          analytic.py:23-29
+ *   FS_EVAL_GROUPED_GEMM    [routed, active, d_model, d_ff, n_matrices, peak_flops,
+ *                            mem_bw, overhead_us, dtype] -> [us]   analytic.py:56-71
+ *   FS_EVAL_COLLECTIVE_INT  [kind (0 all_to_all, 1 all_reduce, 2 all_gather),
+ *   FS_EVAL_COLLECTIVE_FLT   bytes_per_rank, n_ranks, latency_s, bandwidth_bps]
+ *                           -> [s]  topology.py:367-394 (int or float bytes)
+ *   FS_EVAL_TRANSFER        [bytes, latency_s, bandwidth_bps] -> [s]  topology.py:241-243
+ *   FS_EVAL_MOE_LAYER       [E, top_k, ep, moe_tp, n_matrices, T, d_model,
+ *                            expert_d_ff, dtype, latency_s, bandwidth_bps,
+ *                            peak_flops, mem_bw, overhead_us, counts[E]]
+ *                           -> [total_us, expert_us / mean(per_rank_us)]  moe.py:69-128
+ *   FS_EVAL_CUDA_*          CUDA's own libm for the same four functions (the
+ *                           simulator never calls it; tests use it to show where
+ *                           it would have diverged from the host) */
+enum fs_eval_fn {
+  FS_EVAL_EXP = 1, FS_EVAL_LOG = 2, FS_EVAL_LOG1P = 3, FS_EVAL_POW = 4,
+  FS_EVAL_LINEAR = 5, FS_EVAL_GROUPED_GEMM = 6, FS_EVAL_COLLECTIVE_INT = 7,
+  FS_EVAL_COLLECTIVE_FLT = 8, FS_EVAL_TRANSFER = 9, FS_EVAL_MOE_LAYER = 10,
+  FS_EVAL_CUDA_EXP = 11, FS_EVAL_CUDA_LOG = 12, FS_EVAL_CUDA_LOG1P = 13, FS_EVAL_CUDA_POW = 14
+};
+int fs_eval(fs_engine* e, int32_t fn, const double* in, int32_t in_stride, int64_t n,
+            double* out, int32_t out_stride, int32_t* status);
 
 #ifdef __cplusplus
 }

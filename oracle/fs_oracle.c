@@ -1975,6 +1975,21 @@ double fso_pysum(const double* x, int n) {
   return pysum_result(&s);
 }
 
+/* The system libm's exp / log / log1p / pow (the functions numpy's distributions.c
+ * calls) over arrays: fn 1 exp, 2 log, 3 log1p, 4 pow(x[i], y[i]). The device's
+ * restatement (fs_glibm.h) is tested against these. */
+void fso_libm(int fn, const double* x, const double* y, double* out, int64_t n) {
+  for (int64_t i = 0; i < n; i++) {
+    switch (fn) {
+      case 1: out[i] = exp(x[i]); break;
+      case 2: out[i] = log(x[i]); break;
+      case 3: out[i] = log1p(x[i]); break;
+      case 4: out[i] = pow(x[i], y[i]); break;
+      default: out[i] = 0.0;
+    }
+  }
+}
+
 int fso_struct_sizes(int64_t* out, int n) {
   const int64_t s[] = {(int64_t)sizeof(fs_cost_ctx),     (int64_t)sizeof(fs_seed_prefix),
                        (int64_t)sizeof(fs_replica_desc), (int64_t)sizeof(fs_instance_desc),

@@ -71,6 +71,7 @@ def load():
                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, vp]
     lib.fso_pysum.restype = ctypes.c_double
     lib.fso_pysum.argtypes = [vp, ctypes.c_int]
+    lib.fso_libm.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_int64]
     abi.check_sizes(lib, "fso_struct_sizes")
     _lib = lib
     return lib
@@ -166,6 +167,17 @@ def generate_workload(descs):
     load().fso_generate_workload(abi.ptr(descs), len(descs), abi.ptr(arr), abi.ptr(pr),
                                  abi.ptr(out), abi.ptr(rk), abi.ptr(st))
     return arr[:n_total], pr[:n_total], out[:n_total], rk[:n_total], st[:len(descs)]
+
+
+def libm(fn: str, x, y=None) -> np.ndarray:
+    """The host C library's exp / log / log1p / pow elementwise (glibc, as numpy's
+    distributions.c calls them)."""
+    code = {"exp": 1, "log": 2, "log1p": 3, "pow": 4}[fn]
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(x if y is None else y, dtype=np.float64)
+    out = np.zeros_like(x)
+    load().fso_libm(code, x.ctypes.data, y.ctypes.data, out.ctypes.data, len(x))
+    return out
 
 
 def pysum(xs) -> float:

@@ -55,7 +55,7 @@ struct fs_engine {
       lg_events, lg_ecount;
   // cost-model scratch
   DevBuf c_q, c_kv, c_off, c_dec, c_out, c_status, c_tok, c_seed, c_counts, c_pidx, c_mb, c_steps,
-      c_layers, c_seeds, c_pf, c_mid, c_scratch;
+      c_layers, c_seeds, c_pf, c_mid, c_scratch, c_ein, c_eout;
   // workload generation
   DevBuf g_desc, g_arr, g_pr, g_out, g_rank, g_st;
   // learned models (persist across stages)
@@ -617,6 +617,28 @@ int fs_route_tokens(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, 
   FS_CHECK(cudaMemcpyAsync(counts_out, e->c_counts.p, 4 * (size_t)n_calls * num_experts,
                            cudaMemcpyDeviceToHost, s));
   FS_CHECK(cudaMemcpyAsync(status, e->c_status.p, 4 * (size_t)n_calls, cudaMemcpyDeviceToHost, s));
+  FS_CHECK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fs_eval(fs_engine* e, int32_t fn, const double* in, int32_t in_stride, int64_t n,
+            double* out, int32_t out_stride, int32_t* status) {
+  if (!e) return 1;
+  if (n < 0 || in_stride < 1 || out_stride < 1) { e->err = "fs_eval: bad sizes"; return 1; }
+  FS_CHECK(cudaSetDevice(e->device));
+  cudaStream_t s = e->stream;
+  FS_CHECK(upload(e->c_ein, in, (size_t)n * in_stride, s));
+  FS_CHECK(e->c_eout.ensure((size_t)std::max<int64_t>(n, 1) * out_stride * 8));
+  FS_CHECK(e->c_status.ensure((size_t)std::max<int64_t>(n, 1) * 4));
+  FS_CHECK(cudaMemsetAsync(e->c_eout.p, 0, (size_t)std::max<int64_t>(n, 1) * out_stride * 8, s));
+  e->last_launches = fs::launch_eval(fn, e->c_ein.as<double>(), in_stride, n,
+                                     e->c_eout.as<double>(), out_stride,
+                                     e->c_status.as<int32_t>(), e->n_sms, s);
+  FS_CHECK(cudaGetLastError());
+  if (n > 0) {
+    FS_CHECK(cudaMemcpyAsync(out, e->c_eout.p, (size_t)n * out_stride * 8, cudaMemcpyDeviceToHost, s));
+    FS_CHECK(cudaMemcpyAsync(status, e->c_status.p, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  }
   FS_CHECK(cudaStreamSynchronize(s));
   return 0;
 }

@@ -528,9 +528,8 @@ __global__ void workload_kernel(const fs_workload_desc* __restrict__ w, int n,
     } else if (L.kind == FS_LEN_UNIFORM) {
       v = np_integer_dev(s, L.lo, L.hi);
     } else if (L.kind == FS_LEN_LOGNORMAL) {
-      // random_lognormal = exp(random_normal(mu, sigma)); CUDA's exp (<= 1 ulp) vs
-      // glibc's can only matter when the draw sits on a .5 rounding boundary
-      double x = rint(exp(L.mu + L.sigma * np_std_normal(s.g)));
+      // random_lognormal = exp(random_normal(mu, sigma)) with glibc's exp (fs_glibm.h)
+      double x = rint(glm_exp(L.mu + L.sigma * np_std_normal(s.g)));
       x = x < (double)L.lo ? (double)L.lo : x;
       x = x > (double)L.hi ? (double)L.hi : x;
       v = (int64_t)x;
@@ -799,6 +798,87 @@ __global__ void seeds_kernel(const fs_seed_prefix* pf, const uint32_t* mid, cons
   ints[k++] = steps[i];
   ints[k++] = layers[i];
   out[i] = sha256_tail_first_word(mid + (int64_t)pidx[i] * 8, p->len / 64, p->bytes, p->len, ints, k);
+}
+
+// fs_eval (diagnostics): the pure functions the simulator composes, one record
+// per warp, through the same device functions sim_kernel calls. Integers arrive
+// as exact doubles. Layouts: include/frontier_b200.h, enum fs_eval_fn.
+__device__ __forceinline__ int64_t evi(double x) { return (int64_t)x; }
+__global__ void eval_kernel(int fn, const double* __restrict__ in, int in_stride, int64_t n,
+                            double* __restrict__ out, int out_stride, int32_t* __restrict__ status) {
+  __shared__ int counts[4][FS_MAX_EXPERTS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = (int64_t)blockIdx.x * 4 + w, nw = (int64_t)gridDim.x * 4;
+  for (int64_t i = warp; i < n; i += nw) {
+    const double* a = in + i * in_stride;
+    double* o = out + i * out_stride;
+    int st = FS_OK;
+    if (fn == FS_EVAL_MOE_LAYER) {
+      // [E, k, ep, moe_tp, n_matrices, T, d_model, expert_d_ff, dtype, latency_s,
+      //  bandwidth_bps, peak_flops, mem_bw, overhead_us, counts[E]] -> [total_us, ratio]
+      const int E = (int)a[0];
+      if (E < 1 || E > FS_MAX_EXPERTS) {
+        st = FS_ERR_CAPACITY;
+      } else {
+        for (int e = lane; e < E; e += 32) counts[w][e] = (int)a[14 + e];
+        __syncwarp();
+        fs_cost_ctx c;
+        c.peak_flops = a[11]; c.mem_bw = a[12]; c.kernel_overhead_us = a[13];
+        c.tp = 1; c.ep = (int)a[2]; c.moe_tp = (int)a[3]; c.pp = 1;
+        double total = 0.0, ratio = 0.0;
+        st = moe_layer_warp(lane, counts[w], evi(a[5]), E, (int)a[1], (int)a[6], (int)a[7],
+                            (int)a[4], (int)a[8], (int)a[2], (int)a[3], a[9], a[10], c, &total,
+                            &ratio);
+        if (lane == 0) { o[0] = total; o[1] = ratio; }
+        __syncwarp();
+      }
+    } else if (lane == 0) {
+      switch (fn) {
+        case FS_EVAL_EXP: o[0] = glm_exp(a[0]); break;
+        case FS_EVAL_LOG: o[0] = glm_log(a[0]); break;
+        case FS_EVAL_LOG1P: o[0] = glm_log1p(a[0]); break;
+        case FS_EVAL_POW: o[0] = glm_pow(a[0], a[1]); break;
+        case FS_EVAL_CUDA_EXP: o[0] = exp(a[0]); break;  // CUDA libm, for comparison only
+        case FS_EVAL_CUDA_LOG: o[0] = log(a[0]); break;
+        case FS_EVAL_CUDA_LOG1P: o[0] = log1p(a[0]); break;
+        case FS_EVAL_CUDA_POW: o[0] = pow(a[0], a[1]); break;
+        case FS_EVAL_LINEAR: {  // [m, n, k, peak_flops, mem_bw, overhead_us, dtype]
+          fs_cost_ctx c;
+          c.peak_flops = a[3]; c.mem_bw = a[4]; c.kernel_overhead_us = a[5];
+          o[0] = linear_us(evi(a[0]), evi(a[1]), evi(a[2]), c, (int)a[6]);
+          break;
+        }
+        case FS_EVAL_GROUPED_GEMM: {  // [routed, active, d_model, d_ff, n_matrices, peak, bw, ovh, dtype]
+          fs_cost_ctx c;
+          c.peak_flops = a[5]; c.mem_bw = a[6]; c.kernel_overhead_us = a[7];
+          o[0] = grouped_gemm_us(evi(a[0]), evi(a[1]), evi(a[2]), evi(a[3]), (int)a[4], c,
+                                 (int)a[8]);
+          break;
+        }
+        case FS_EVAL_COLLECTIVE_INT:  // [kind, bytes_per_rank, n_ranks, latency_s, bandwidth_bps]
+          o[0] = collective_int((int)a[0] == 1, evi(a[1]), (int)a[2], a[3], a[4]);
+          break;
+        case FS_EVAL_COLLECTIVE_FLT:
+          o[0] = collective_flt((int)a[0] == 1, a[1], (int)a[2], a[3], a[4]);
+          break;
+        case FS_EVAL_TRANSFER:  // [bytes, latency_s, bandwidth_bps]
+          o[0] = transfer_s(evi(a[0]), a[1], a[2]);
+          break;
+        default: st = FS_ERR_VALUE;
+      }
+    }
+    if (lane == 0) status[i] = st;
+  }
+}
+
+int launch_eval(int fn, const double* in, int in_stride, int64_t n, double* out, int out_stride,
+                int32_t* status, int n_sms, void* stream) {
+  if (n <= 0) return 0;
+  int64_t blocks = (n + 3) / 4;
+  if (blocks > 8 * n_sms) blocks = 8 * n_sms;
+  eval_kernel<<<(int)blocks, 128, 0, (cudaStream_t)stream>>>(fn, in, in_stride, n, out,
+                                                             out_stride, status);
+  return 1;
 }
 
 int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int32_t* pidx,

@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "../../include/frontier_b200.h"
+#include "fs_glibm.h"  // glibc exp/log/log1p/pow, bit for bit
 
 #define FS_FULL 0xffffffffu
 
@@ -94,6 +95,12 @@ __device__ __forceinline__ double collective_flt(bool all_reduce, double bpr, in
   wire = wire / bw;
   if (all_reduce) return 2.0 * lat + 2.0 * wire;
   return lat + wire;
+}
+
+// topology.py:241-243 transfer_time(bytes, link) = alpha + bytes / beta (seconds);
+// integer bytes (exact below 2^53)
+__device__ __forceinline__ double transfer_s(int64_t nbytes, double lat, double bw) {
+  return lat + i2d(nbytes) / bw;
 }
 
 // analytic.py:56-71 over one rank's (routed, active) summary

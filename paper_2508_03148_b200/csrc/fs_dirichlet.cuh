@@ -25,11 +25,12 @@
 //     rows are reduced to their k smallest (k+1 kept to detect an exact
 //     boundary tie, like the uniform router) and tallied.
 //
-// fp64 notes: pow / log / exp / log1p are CUDA's (documented 1-2 ulp), glibc's in
-// numpy. They only enter the rare slow path and the popularity vector; the
-// output is integer counts, which agree unless two keys of a row sit within a
-// few ulp of each other at the selection boundary (tests pin the counts against
-// numpy's and the reference's on hundreds of calls).
+// fp64 notes: pow / log / exp / log1p are glibc's own algorithms as numpy's
+// distributions.c gets them from libm (fs_glibm.h: the x86-64 FMA variants,
+// tables read from the installed libm), so every accept/reject comparison --
+// and with it the number of words each variate consumes -- is decided exactly
+// as on the host. Everything else is IEEE add/mul/div/sqrt in numpy's order
+// (-fmad=false).
 #pragma once
 #include "fs_device.cuh"
 #include "fs_engine.h"
@@ -66,9 +67,9 @@ static __device__ __noinline__ double np_std_exponential(NpStream& g) {
     ri >>= 8;
     const double x = (double)ri * zig(fs_zig_we, idx);
     if (ri < zigu(fs_zig_ke, idx)) return x;
-    if (idx == 0) return FS_ZIG_EXP_R - log1p(-g.next_double());
+    if (idx == 0) return FS_ZIG_EXP_R - glm_log1p(-g.next_double());
     if ((zig(fs_zig_fe, idx - 1) - zig(fs_zig_fe, idx)) * g.next_double() + zig(fs_zig_fe, idx) <
-        exp(-x))
+        glm_exp(-x))
       return x;
   }
 }
@@ -85,14 +86,14 @@ static __device__ __noinline__ double np_std_normal(NpStream& g) {
     if (rabs < zigu(fs_zig_ki, idx)) return x;
     if (idx == 0) {
       for (;;) {
-        const double xx = -FS_ZIG_NOR_INV_R * log1p(-g.next_double());
-        const double yy = -log1p(-g.next_double());
+        const double xx = -FS_ZIG_NOR_INV_R * glm_log1p(-g.next_double());
+        const double yy = -glm_log1p(-g.next_double());
         if (yy + yy > xx * xx)
           return ((rabs >> 8) & 0x1) ? -(FS_ZIG_NOR_R + xx) : FS_ZIG_NOR_R + xx;
       }
     } else {
       if (((zig(fs_zig_fi, idx - 1) - zig(fs_zig_fi, idx)) * g.next_double() +
-           zig(fs_zig_fi, idx)) < exp(-0.5 * x * x))
+           zig(fs_zig_fi, idx)) < glm_exp(-0.5 * x * x))
         return x;
     }
   }
@@ -106,11 +107,11 @@ static __device__ __noinline__ double np_std_gamma(NpStream& g, double shape) {
       const double U = g.next_double();
       const double V = np_std_exponential(g);
       if (U <= 1.0 - shape) {
-        const double X = pow(U, 1. / shape);
+        const double X = glm_pow(U, 1. / shape);
         if (X <= V) return X;
       } else {
-        const double Y = -log((1 - U) / shape);
-        const double X = pow(1.0 - shape + shape * Y, 1. / shape);
+        const double Y = -glm_log((1 - U) / shape);
+        const double X = glm_pow(1.0 - shape + shape * Y, 1. / shape);
         if (X <= (V + Y)) return X;
       }
     }
@@ -126,7 +127,7 @@ static __device__ __noinline__ double np_std_gamma(NpStream& g, double shape) {
     V = V * V * V;
     const double U = g.next_double();
     if (U < 1.0 - 0.0331 * (X * X) * (X * X)) return b * V;
-    if (log(U) < 0.5 * X * X + b * (1. - V + log(V))) return b * V;
+    if (glm_log(U) < 0.5 * X * X + b * (1. - V + glm_log(V))) return b * V;
   }
 }
 
@@ -134,15 +135,15 @@ static __device__ __noinline__ double np_beta(NpStream& g, double a, double b) {
   if (a <= 1.0 && b <= 1.0) {
     for (;;) {  // Johnk
       const double U = g.next_double(), V = g.next_double();
-      const double X = pow(U, 1.0 / a), Y = pow(V, 1.0 / b);
+      const double X = glm_pow(U, 1.0 / a), Y = glm_pow(V, 1.0 / b);
       const double XpY = X + Y;
       if (XpY <= 1.0 && U + V > 0.0) {
         if (XpY > 0) return X / XpY;
-        double logX = log(U) / a, logY = log(V) / b;
+        double logX = glm_log(U) / a, logY = glm_log(V) / b;
         const double logM = logX > logY ? logX : logY;
         logX -= logM;
         logY -= logM;
-        return exp(logX - log(exp(logX) + exp(logY)));
+        return glm_exp(logX - glm_log(glm_exp(logX) + glm_exp(logY)));
       }
     }
   }
@@ -361,10 +362,10 @@ static __device__ __noinline__ int route_dirichlet_warp(int lane, int64_t T, int
       const uint64_t nw = j < 3 ? blk.v[j + 1] : lastw;
       const double U = (double)(nw >> 11) * (1.0 / 9007199254740992.0);
       if (idx == 0) {
-        val[j] = FS_ZIG_EXP_R - log1p(-U);
+        val[j] = FS_ZIG_EXP_R - glm_log1p(-U);
         acc_bits |= 1u << j;
       } else if ((zig(fs_zig_fe, idx - 1) - zig(fs_zig_fe, idx)) * U + zig(fs_zig_fe, idx) <
-                 exp(-x)) {
+                 glm_exp(-x)) {
         val[j] = x;
         acc_bits |= 1u << j;
       }

@@ -138,6 +138,8 @@ int launch_route_tokens(const int64_t* tokens, const uint64_t* seeds, int n, int
 int route_scratch_warps(int n);  // warps (scratch slots) launch_route_tokens uses for n calls
 int launch_workload(const fs_workload_desc* w, int n, int64_t* arrival, int32_t* prompt,
                     int32_t* output, int32_t* rank, int32_t* status, void* stream);
+int launch_eval(int fn, const double* in, int in_stride, int64_t n, double* out, int out_stride,
+                int32_t* status, int n_sms, void* stream);
 int launch_router_seeds(const fs_seed_prefix* pf, const uint32_t* mid, const int32_t* pidx,
                         const int32_t* mb, const int64_t* steps, const int32_t* layers, int n,
                         uint32_t* out, void* stream);

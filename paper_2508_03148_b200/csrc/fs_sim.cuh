@@ -853,13 +853,13 @@ __device__ __noinline__ int learned_moe_layer_warp(const EngineParams& P, Inst& 
           const unsigned m = __ballot_sync(FS_FULL, act);
           if (act) {
             const double pr = (double)cr[e] / sum;
-            plogp[base + __popc(m & ((1u << lane) - 1u))] = pr * log(pr);
+            plogp[base + __popc(m & ((1u << lane) - 1u))] = pr * glm_log(pr);
           }
           base += __popc(m);
         }
         __syncwarp();
         auto term = [&](int64_t i) { return plogp[i]; };
-        ent = -np_pairwise_w(0, nact, term, lane) / log((double)per);
+        ent = -np_pairwise_w(0, nact, term, lane) / glm_log((double)per);
       }
       __syncwarp();
       if (lane == 0) {
@@ -1530,7 +1530,7 @@ __device__ void pd_pump(const EngineParams& P, Inst& I) {
     I.xh++;
     I.events += 1;  // KV_CACHE_TRANSFER_START
     const int64_t nbytes = d->kv_bytes_per_token * prompt;
-    const double sec = d->inter_latency_s + i2d(nbytes) / d->inter_bandwidth_bps;
+    const double sec = transfer_s(nbytes, d->inter_latency_s, d->inter_bandwidth_bps);
     const int64_t t_done = I.now + py_round(sec * 1e9);
     if (tracing(P) && I.lane == 0) {
       const int32_t src = P.home[gi(I, req)];

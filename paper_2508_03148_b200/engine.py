@@ -61,6 +61,7 @@ def load_library(path: str = LIB_PATH):
                                            vp]),
         "fs_generate_workload": (ctypes.c_int, [vp, vp, i32, vp, vp, vp, vp, vp]),
         "fs_router_seeds": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i32, vp]),
+        "fs_eval": (ctypes.c_int, [vp, i32, vp, i32, i64, vp, i32, vp]),
         "fs_set_forests": (ctypes.c_int, [vp, abi.ForestSetC]),
         "fs_attention_forest": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i64, _AttnParamsC, vp]),
         "fs_attention_forest_dev": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, i64, _AttnParamsC,
@@ -194,7 +195,9 @@ def make_log(n_instances: int, spec: LogSpec, sizes: dict | None = None) -> RawL
         sz = np.asarray(sizes[f], dtype=np.int64) if f in sizes else np.full(n_instances, cap, np.int64)
         bases[f] = np.concatenate([[0], np.cumsum(sz)[:-1]]).astype(np.int64) if n_instances \
             else np.zeros(0, np.int64)
-        total[f] = int(sz.sum()) if cap else 0
+        # fs_run_batch copies max_i(base_i + cap) records back (include/frontier_b200.h,
+        # fs_log): with packed regions the last one still needs `cap` slots of room
+        total[f] = int((bases[f] + cap).max()) if cap and n_instances else 0
     log = RawLog(
         spec=spec,
         batches=np.zeros(max(1, total["batch"]), dtype=abi.BATCH_REC),
@@ -443,6 +446,21 @@ class Engine:
                                              abi.ptr(st), abi.ptr(ly), len(pidx), abi.ptr(out)),
                     "fs_router_seeds")
         return out[: len(pidx)]
+
+    EVAL_FNS = {"exp": 1, "log": 2, "log1p": 3, "pow": 4, "linear": 5, "grouped_gemm": 6,
+                "collective_int": 7, "collective_flt": 8, "transfer": 9, "moe_layer": 10,
+                "cuda_exp": 11, "cuda_log": 12, "cuda_log1p": 13, "cuda_pow": 14}
+
+    def eval(self, fn: str, records, out_stride: int = 1):
+        """fs_eval: one pure cost-model / libm function per record on the device
+        (include/frontier_b200.h, enum fs_eval_fn). Returns (out, status)."""
+        rec = np.ascontiguousarray(np.atleast_2d(np.asarray(records, dtype=np.float64)))
+        n, stride = rec.shape
+        out = np.zeros((max(n, 1), out_stride), dtype=np.float64)
+        st = np.zeros(max(n, 1), dtype=np.int32)
+        self._check(self.lib.fs_eval(self.h, self.EVAL_FNS[fn], abi.ptr(rec), stride, n,
+                                     abi.ptr(out), out_stride, abi.ptr(st)), "fs_eval")
+        return out[:n], st[:n]
 
 
 _default_engine: Engine | None = None

@@ -19,7 +19,7 @@ SOURCES = ["fs_engine.cu", "fs_engine_learned.cu", "fs_engine_longrow.cu", "fs_e
            "fs_metrics.cu",
            "fs_costs.cu", "fs_capi.cu"]
 HEADERS = ["fs_device.cuh", "fs_route.cuh", "fs_engine.h", "fs_forest.cuh", "fs_sim.cuh",
-           "fs_dirichlet.cuh", "fs_ziggurat.h"]
+           "fs_dirichlet.cuh", "fs_ziggurat.h", "fs_glibm.h", "fs_glibm_tables.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     *ARCH, "-O3", "-lineinfo", "-std=c++17",

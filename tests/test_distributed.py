@@ -11,6 +11,7 @@ single-process run byte for byte.
 import os
 import pickle
 import socket
+import time
 
 import numpy as np
 import pytest
@@ -51,10 +52,16 @@ def _engine(kind):
     return Engine(0)
 
 
-def _worker(rank, world, port, kind, out):
+def _worker(rank, world, port, kind, out, trace_dir):
+    import faulthandler
+
     import torch.distributed as dist
     from paper_2508_03148_b200.api import simulate, simulate_rows
 
+    # a hung rank dumps its Python stack (read back by _two_ranks) instead of
+    # leaving the test to time out silently
+    tf = open(os.path.join(trace_dir, f"rank{rank}.txt"), "w")
+    faulthandler.dump_traceback_later(240, exit=True, file=tf)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     eng = _engine(kind)
@@ -66,16 +73,35 @@ def _worker(rank, world, port, kind, out):
                               sr.rows.tobytes(), sr.failed, sr.config_hash)))
     dist.barrier()
     dist.destroy_process_group()
+    faulthandler.cancel_dump_traceback_later()
 
 
 def _two_ranks(kind):
+    import queue
+    import tempfile
+
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    trace_dir = tempfile.mkdtemp(prefix="fs_dist_")
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q, trace_dir)) for r in range(2)]
     for p in procs:
         p.start()
-    res = pickle.loads(q.get(timeout=600))
+    deadline = time.monotonic() + 300
+    res = None
+    while res is None and time.monotonic() < deadline:
+        try:
+            res = pickle.loads(q.get(timeout=2))
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    if res is None:
+        for p in procs:
+            p.join(timeout=30)
+        stacks = "".join(open(os.path.join(trace_dir, f)).read()
+                         for f in sorted(os.listdir(trace_dir)))
+        raise AssertionError(f"a rank hung or died (exit codes {[p.exitcode for p in procs]}):"
+                             f"\n{stacks}")
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
