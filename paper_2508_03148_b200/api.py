@@ -9,13 +9,15 @@ the reference's per-point loop over `run_one` (cli.py:82-102, 197-237).
 
 from __future__ import annotations
 
+import gc
 import math
 import time
+from contextlib import contextmanager
 
 import numpy as np
 from dataclasses import dataclass
 
-from .config import DeploymentConfig, parse_config
+from .config import DeploymentConfig, parse_config, parse_many
 from .distributed import gather_rows, lpt_shards, merge_shards
 from .costmodel import check_model_slots_engine
 from . import abi
@@ -76,30 +78,43 @@ def device_request_arrays(configs: list[DeploymentConfig], engine: Engine | None
     reference's ValidationError for invalid distribution parameters, per config,
     through the returned list (an Exception entry)."""
     from .config import ValidationError
+    from .lower import shared_ids
     from .workload import RequestArrays, WorkloadError, workload_descs
     eng = engine or default_engine()
     out: list = [None] * len(configs)
     idx, wl = [], []
+    bad: dict = {}  # distribution objects -> validation error (checked once per template)
     for i, cfg in enumerate(configs):
         if cfg.trace_path is not None:
             continue
-        try:
-            workload_descs([cfg.workload])
-        except WorkloadError as exc:
-            out[i] = ValidationError(str(exc))
+        w = cfg.workload
+        key = (id(w.arrival), id(w.prompt_len), id(w.output_len), w.num_requests)
+        if key not in bad:
+            try:
+                w.validate()
+                bad[key] = None
+            except WorkloadError as exc:
+                bad[key] = ValidationError(str(exc))
+        if bad[key] is not None:
+            out[i] = bad[key]
             continue
         idx.append(i)
-        wl.append(cfg.workload)
+        wl.append(w)
     if wl:
         descs = workload_descs(wl)
         arr, pr, ou, _, st = eng.generate_workload(descs)
+        pr = pr.astype(np.int64)
+        ou = ou.astype(np.int64)
+        offs = descs["out_offset"].tolist()
+        ns = descs["n_requests"].tolist()
         for j, i in enumerate(idx):
             if st[j] != 0:
                 out[i] = ValidationError(f"workload generation failed (status {int(st[j])})")
                 continue
-            o, n = int(descs[j]["out_offset"]), int(descs[j]["n_requests"])
-            out[i] = RequestArrays([f"r{k}" for k in range(n)], arr[o:o + n].copy(),
-                                   pr[o:o + n].astype(np.int64), ou[o:o + n].astype(np.int64))
+            o, n = offs[j], ns[j]
+            # ids r0..r{n-1}: synthetic arrivals are non-decreasing, so generation order
+            # is request order (workload_descs); views into the generated arrays
+            out[i] = RequestArrays(shared_ids(n), arr[o:o + n], pr[o:o + n], ou[o:o + n])
     return out
 
 
@@ -175,18 +190,20 @@ def config_cost(config: DeploymentConfig) -> int:
     return int(work)
 
 
-def _parse(c, base_dir: str):
-    if isinstance(c, (DeploymentConfig, Failure)):
-        return c
-    try:
-        return parse_config(c, base_dir=base_dir)
-    except Exception as exc:  # config-time failures (cli.py:229-233)
-        return Failure(exc)
+def parse_all(configs: list, base_dir: str = ".") -> list:
+    """Parsed DeploymentConfigs, or Failure entries for the points that fail to
+    parse (cli.py:229-233); documents that differ only in their seeds share one
+    parse and validation (config.parse_many)."""
+    out = list(configs)
+    idx = [i for i, c in enumerate(configs) if not isinstance(c, Failure)]
+    for i, p in zip(idx, parse_many([configs[i] for i in idx], base_dir, on_error=Failure)):
+        out[i] = p
+    return out
 
 
 def shard_plan(configs: list, world: int, base_dir: str = "."):
     """(parsed configs or Failures, LPT shards over ranks): same on every rank."""
-    parsed = [_parse(c, base_dir) for c in configs]
+    parsed = parse_all(configs, base_dir)
     costs = [config_cost(p) if isinstance(p, DeploymentConfig) else 0 for p in parsed]
     return parsed, lpt_shards(costs, world)
 
@@ -207,6 +224,20 @@ def _simulate_sharded(dist, configs, engine, base_dir, device_workload, expert_i
     return out
 
 
+@contextmanager
+def _gc_paused():
+    """A batch allocates a few objects per request and instance and frees none of
+    them until it returns; the cyclic collector's passes over that growing heap
+    are pure overhead here (reference counting still frees everything)."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()
+
+
 def simulate(configs: list, engine: Engine | None = None, base_dir: str = ".",
              device_workload: bool = False, expert_imbalance: bool = True,
              distributed: bool | None = None) -> list[MetricsBundle | Failure]:
@@ -222,11 +253,15 @@ def simulate(configs: list, engine: Engine | None = None, base_dir: str = ".",
     if dist is not None:
         return _simulate_sharded(dist, configs, engine, base_dir, device_workload,
                                  expert_imbalance)
+    with _gc_paused():
+        return _simulate_local(configs, engine, base_dir, device_workload, expert_imbalance)
+
+
+def _simulate_local(configs, engine, base_dir, device_workload, expert_imbalance):
     out: list[MetricsBundle | Failure | None] = [None] * len(configs)
     specs, where = [], []
     parsed: list = [None] * len(configs)
-    for i, c in enumerate(configs):
-        p = c if isinstance(c, Failure) else _parse(c, base_dir)
+    for i, p in enumerate(parse_all(configs, base_dir)):
         if isinstance(p, Failure):
             out[i] = p
         else:
@@ -291,6 +326,11 @@ def simulate_rows(configs: list, engine: Engine | None = None, base_dir: str = "
     """simulate() reduced to the fixed-size metric rows, which is all a sweep's CSV and
     frontier read. Multi-GPU: LPT shards per rank, one all-gather of the rows over
     the process group (NCCL on the B200 box) plus the failure texts."""
+    with _gc_paused():
+        return _simulate_rows(configs, engine, base_dir, device_workload, distributed)
+
+
+def _simulate_rows(configs, engine, base_dir, device_workload, distributed) -> SweepRows:
     dist = process_group(distributed)
     world, rank = (dist.get_world_size(), dist.get_rank()) if dist is not None else (1, 0)
     parsed, shards = shard_plan(configs, world, base_dir)

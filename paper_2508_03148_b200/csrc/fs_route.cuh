@@ -120,8 +120,13 @@ __device__ int route_uniform_warp_k(int lane, int64_t T, int E, int k, uint64_t 
 __device__ inline int route_uniform_warp(int lane, int64_t T, int E, int k, uint64_t k0,
                                          uint64_t k1, int* counts) {
   if (k + 1 <= 4) return route_uniform_warp_k<4>(lane, T, E, k, k0, k1, counts);
+#if !defined(FS_KCAP_MAX) || FS_KCAP_MAX > 4
   if (k + 1 <= 9) return route_uniform_warp_k<9>(lane, T, E, k, k0, k1, counts);
+#endif
+#if !defined(FS_KCAP_MAX) || FS_KCAP_MAX > 9
   return route_uniform_warp_k<FS_MAX_TOPK + 1>(lane, T, E, k, k0, k1, counts);
+#endif
+  return FS_ERR_INTERNAL;
 }
 
 // moe_layer_latency from a tally in shared memory. All lanes return the same

@@ -55,6 +55,9 @@
 #ifndef FS_TOPK_BRANCHFREE  // insert every key (no threshold test): in a warp some lane
 #define FS_TOPK_BRANCHFREE 0  // almost always inserts, so the test only adds instructions
 #endif
+#ifndef FS_KCAP_MAX  // largest top-(k+1) list compiled in (4: k <= 3 only -- a variant for
+#define FS_KCAP_MAX 17  // small-k MoE batches, whose routing then needs fewer registers)
+#endif
 #ifndef FS_LONG_ROW_UNROLL  // unrolled Philox rounds for long row segments (>= 64 draws):
 #define FS_LONG_ROW_UNROLL 0  // C4 EP 430 -> 373 ms, but the C5 sweep 272 -> ~300 ms (code size)
 #endif
@@ -564,8 +567,12 @@ __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* cou
                               int lane, int* tally, bool publish) {
   const int k = __ldcg(&job->k);
   if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane, tally);
+#if FS_KCAP_MAX > 4
   else if (k + 1 <= 9) process_chunk_k<9>(P, job, counts, c, lane, tally);
+#endif
+#if FS_KCAP_MAX > 9
   else process_chunk_k<FS_MAX_TOPK + 1>(P, job, counts, c, lane, tally);
+#endif
   __syncwarp();
   if (publish && lane == 0) red_add_release_i32(&job->done, 1);
 }

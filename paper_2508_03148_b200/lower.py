@@ -127,15 +127,11 @@ class Lowered:
         return len(self.arrival)
 
 
-def check_spec(sp: InstanceSpec) -> None:
-    """The per-instance checks the reference makes inside make_simulation
-    (base.py:71-111, af.py:381-392, cluster.py:108-118) plus the engine's
-    capacity limits. simulate() runs this per point, so a bad point becomes a
-    Failure row (cli.py:229-233) and lower() cannot raise for the others."""
+def _check_static(sp: InstanceSpec) -> int:
+    """The seed- and request-independent checks of check_spec; returns the longest
+    replica key (for the router-seed prefix bound)."""
     dep, model = sp.deployment, sp.deployment.model
     sp.policy.validate()
-    if len(set(sp.requests.ids)) != len(sp.requests.ids):
-        raise SimulationError("duplicate request id")
     layout = replica_layout(dep)
     if not layout:
         raise SimulationError(f"{dep.mode} deployment has no serving replicas")
@@ -143,8 +139,6 @@ def check_spec(sp: InstanceSpec) -> None:
         raise EngineCapacityError(f"{len(layout)} replicas exceed {abi.MAX_REPLICAS}")
     if model.moe is not None and model.moe.num_experts > abi.MAX_EXPERTS:
         raise EngineCapacityError(f"{model.moe.num_experts} experts exceed {abi.MAX_EXPERTS}")
-    for ri in layout:
-        _prefix(f"{sp.seed}:{ri.key}:mb")  # router-seed prefix length
     if dep.mode == "af":
         (sp.af or AfPipelineConfig()).validate()
         attn = dep.clusters_with_role("attention")
@@ -157,39 +151,61 @@ def check_spec(sp: InstanceSpec) -> None:
                       (sp.grouped_gemm_model, "grouped_gemm_v1")):
         if m is not None and m.schema == schema and m.n_trees > abi.MAX_FOREST_TREES:
             raise EngineCapacityError(f"{m.path}: {m.n_trees} trees exceed {abi.MAX_FOREST_TREES}")
+    return max(len(ri.key.encode("utf-8")) for ri in layout)
 
 
-def lower(specs: list[InstanceSpec]) -> Lowered:
-    n = len(specs)
-    descs = np.zeros(n, dtype=abi.INSTANCE_DESC)
-    reps: list[tuple] = []
-    prefixes: list[np.void] = []
-    trace: list[int] = []
-    arr_parts, p_parts, o_parts, rank_parts = [], [], [], []
-    replica_keys, request_ids = [], []
-    req_off = 0
-    forests = ForestSet()
-    for i, sp in enumerate(specs):
+def check_spec(sp: InstanceSpec) -> None:
+    """The per-instance checks the reference makes inside make_simulation
+    (base.py:71-111, af.py:381-392, cluster.py:108-118) plus the engine's
+    capacity limits. simulate() runs this per point, so a bad point becomes a
+    Failure row (cli.py:229-233) and lower() cannot raise for the others.
+    The seed-independent part is memoised on the Deployment (sweep points of one
+    config share it; the memo keeps the objects it keys on alive)."""
+    memo = sp.deployment.__dict__.setdefault("_spec_checks", {})
+    key = (sp.policy, sp.af, id(sp.attention_model), id(sp.grouped_gemm_model))
+    hit = memo.get(key)
+    if hit is None:
+        try:
+            longest = _check_static(sp)
+        except Exception as exc:
+            longest = exc
+        hit = memo[key] = (sp.attention_model, sp.grouped_gemm_model, longest)
+    if isinstance(hit[2], Exception):
+        raise hit[2]
+    ids = sp.requests.ids
+    if ids is not _RANKS_CACHE.get(len(ids), (None,))[0] and len(set(ids)) != len(ids):
+        raise SimulationError("duplicate request id")
+    plen = len(str(sp.seed)) + hit[2] + 4  # "{seed}:{key}:mb"
+    if plen > abi.MAX_PREFIX_BYTES:
+        _prefix(f"{sp.seed}:{'x' * hit[2]}:mb")  # raises with the reference-style message
+    sp.__dict__["_checked"] = True
+
+
+class _Template:
+    """Everything `lower` derives from an instance that does not depend on its seed
+    or its requests: the descriptor row, the replica rows (prefix indices relative
+    to the instance's first prefix), the replica keys and trace counts. A sweep's
+    config x seed points share one per config (parse_many shares the objects)."""
+
+    __slots__ = ("desc", "reps", "keys", "prefix_suffix", "trace", "af")
+
+    def __init__(self, sp: InstanceSpec, forests: ForestSet) -> None:
         dep, model, pol = sp.deployment, sp.deployment.model, sp.policy
-        check_spec(sp)
         layout = replica_layout(dep)
-        d = descs[i]
+        d = np.zeros((), dtype=abi.INSTANCE_DESC)
         d["mode"] = abi.MODE[dep.mode]
-        d["n_requests"] = len(sp.requests)
-        d["req_offset"] = req_off
         d["n_replicas"] = len(layout)
-        d["replica_offset"] = len(reps)
         for f in ("num_layers", "d_model", "d_ff", "num_query_heads", "num_kv_heads", "head_dim",
                   "dtype_bytes"):
             d[f] = getattr(model, f)
         d["ffn_matrices"] = model.ffn_matrices
         if model.moe is not None:
+            if model.moe.num_experts > abi.MAX_EXPERTS:
+                raise EngineCapacityError(f"{model.moe.num_experts} experts exceed {abi.MAX_EXPERTS}")
             d["has_moe"] = 1
             d["num_experts"] = model.moe.num_experts
             d["top_k"] = model.moe.top_k
             d["expert_d_ff"] = model.moe.expert_d_ff
-            if model.moe.num_experts > abi.MAX_EXPERTS:
-                raise EngineCapacityError(f"{model.moe.num_experts} experts exceed {abi.MAX_EXPERTS}")
         d["admission"] = abi.ADMISSION[pol.admission]
         d["priority_key"] = abi.PRIORITY_KEY[pol.priority_key]
         d["max_num_seqs"] = pol.max_num_seqs
@@ -199,10 +215,8 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
         rt = sp.routing
         d["routing_policy"] = abi.ROUTING[rt.policy]
         d["routing_alpha"] = rt.alpha
-        d["trace_offset"] = len(trace)
-        if rt.trace_counts:
-            d["n_trace_counts"] = len(rt.trace_counts)
-            trace.extend(int(c) for c in rt.trace_counts)
+        self.trace = [int(c) for c in rt.trace_counts] if rt.trace_counts else []
+        d["n_trace_counts"] = len(self.trace)
         net = dep.network
         d["intra_latency_s"] = net.intra_replica.latency_s
         d["intra_bandwidth_bps"] = net.intra_replica.bandwidth_bps
@@ -211,29 +225,14 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
         d["kv_bytes_per_token"] = kv_bytes_per_token(model)
         d["max_events"] = sp.max_events
         d["total_gpus"] = dep.total_gpus
-        for slot, model, schema in (("attn_forest", sp.attention_model, "attention_v1"),
-                                    ("gg_forest", sp.grouped_gemm_model, "grouped_gemm_v1")):
-            if model is not None and model.schema == schema and model.n_trees > abi.MAX_FOREST_TREES:
+        for slot, m, schema in (("attn_forest", sp.attention_model, "attention_v1"),
+                                ("gg_forest", sp.grouped_gemm_model, "grouped_gemm_v1")):
+            if m is not None and m.schema == schema and m.n_trees > abi.MAX_FOREST_TREES:
                 raise EngineCapacityError(
-                    f"{model.path}: {model.n_trees} trees exceed {abi.MAX_FOREST_TREES}")
-            d[slot] = forest_slot(forests, model, schema)
-        d["est_cost"] = _estimate_cost(sp)
-        keys = [ri.key for ri in layout]
-        key_rank = {k: r for r, k in enumerate(sorted(keys))}
-        for ri in layout:
-            c = ri.cluster
-            p = c.parallelism
-            pidx = len(prefixes)
-            prefixes.append(_prefix(f"{sp.seed}:{ri.key}:"))
-            pmb = -1
-            if dep.mode == "af":
-                cost = _cost(c.hardware, p.attn_tp, 1, 1, p.pp)
-                pmb = len(prefixes)
-                prefixes.append(_prefix(f"{sp.seed}:{ri.key}:mb"))
-            else:
-                cost = _cost(c.hardware, p.tp, p.ep, p.tp, p.pp)
-            reps.append((abi.ROLE[ri.role], key_rank[ri.key], c.kv_pool_tokens, cost, pidx, pmb))
-        if dep.mode == "af":
+                    f"{m.path}: {m.n_trees} trees exceed {abi.MAX_FOREST_TREES}")
+            d[slot] = forest_slot(forests, m, schema)
+        self.af = dep.mode == "af"
+        if self.af:
             af = sp.af or AfPipelineConfig()
             af.validate()
             attn = dep.clusters_with_role("attention")
@@ -247,21 +246,146 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
             d["af_attn_dp"] = pa.attn_dp
             d["af_attn"] = _cost(attn[0].hardware, pa.attn_tp, 1, 1, pa.pp)
             d["af_ffn"] = _cost(ffn[0].hardware, pf.moe_tp, pf.moe_ep, pf.moe_tp, pf.pp)
-        r = sp.requests
-        arr_parts.append(np.asarray(r.arrival_ns, dtype=np.int64))
-        p_parts.append(np.asarray(r.prompt, dtype=np.int32))
-        o_parts.append(np.asarray(r.output, dtype=np.int32))
-        rank_parts.append(_id_ranks(r.ids))
-        replica_keys.append(keys)
-        request_ids.append(r.ids)
-        req_off += len(r)
-    replicas = np.array(reps, dtype=abi.REPLICA_DESC) if reps else np.zeros(0, abi.REPLICA_DESC)
-    pref = np.array(prefixes, dtype=abi.SEED_PREFIX) if prefixes else np.zeros(0, abi.SEED_PREFIX)
-    cat = lambda parts, dt: np.concatenate(parts).astype(dt) if parts else np.zeros(0, dt)  # noqa: E731
+        self.desc = d
+        self.keys = [ri.key for ri in layout]
+        key_rank = {k: r for r, k in enumerate(sorted(self.keys))}
+        reps, suffix = [], []
+        for ri in layout:
+            c, p = ri.cluster, ri.cluster.parallelism
+            pidx = len(suffix)
+            suffix.append(f":{ri.key}:")
+            pmb = -1
+            if self.af:
+                cost = _cost(c.hardware, p.attn_tp, 1, 1, p.pp)
+                pmb = len(suffix)
+                suffix.append(f":{ri.key}:mb")
+            else:
+                cost = _cost(c.hardware, p.tp, p.ep, p.tp, p.pp)
+            reps.append((abi.ROLE[ri.role], key_rank[ri.key], c.kv_pool_tokens, cost, pidx, pmb))
+        self.reps = np.array(reps, dtype=abi.REPLICA_DESC)
+        self.prefix_suffix = suffix  # prefix text = f"{seed}{suffix}"
+
+
+def _template_key(sp: InstanceSpec) -> tuple:
+    return (id(sp.deployment), id(sp.policy), id(sp.routing), id(sp.af),
+            id(sp.attention_model), id(sp.grouped_gemm_model), sp.max_events)
+
+
+_RANKS_CACHE: dict[int, tuple[list[str], np.ndarray]] = {}
+
+
+def shared_ids(n: int) -> list[str]:
+    """The id list ["r0", ..., "r{n-1}"] of a generated workload, one shared list per
+    n (treated as immutable), with its str-order ranks computed once."""
+    hit = _RANKS_CACHE.get(n)
+    if hit is None:
+        ids = [f"r{k}" for k in range(n)]
+        hit = _RANKS_CACHE[n] = (ids, _id_ranks(ids))
+    return hit[0]
+
+
+def _ranks_of(ids: list[str]) -> np.ndarray:
+    """_id_ranks, cached for the generated id lists r0..r{n-1} (shared lists)."""
+    hit = _RANKS_CACHE.get(len(ids))
+    if hit is not None and hit[0] is ids:
+        return hit[1]
+    return _id_ranks(ids)
+
+
+def lower(specs: list[InstanceSpec]) -> Lowered:
+    """Pack instances for fs_run_batch. Seed-independent parts are built once per
+    template (_Template); per instance only offsets, seeds' router-seed prefixes
+    and the request arrays are added, mostly as whole-array numpy operations."""
+    n = len(specs)
+    forests = ForestSet()
+    templates: dict[tuple, _Template] = {}
+    tmpl_of: list[_Template] = []
+    for sp in specs:
+        if not getattr(sp, "_checked", False):
+            check_spec(sp)
+        key = _template_key(sp)
+        t = templates.get(key)
+        if t is None:
+            t = templates[key] = _Template(sp, forests)
+        tmpl_of.append(t)
+    descs = np.zeros(n, dtype=abi.INSTANCE_DESC)
+    uniq = list({id(t): t for t in tmpl_of}.values())
+    pos = {id(t): j for j, t in enumerate(uniq)}
+    which = np.fromiter((pos[id(t)] for t in tmpl_of), dtype=np.int64, count=n)
+    if n:
+        tdesc = np.zeros(len(uniq), dtype=abi.INSTANCE_DESC)
+        for j, t in enumerate(uniq):
+            tdesc[j] = t.desc
+        descs[:] = tdesc[which]
+    n_req = np.fromiter((len(sp.requests) for sp in specs), dtype=np.int64, count=n)
+    n_rep = descs["n_replicas"].astype(np.int64)
+    req_off = np.concatenate([[0], np.cumsum(n_req)[:-1]]) if n else n_req
+    rep_off = np.concatenate([[0], np.cumsum(n_rep)[:-1]]) if n else n_rep
+    descs["n_requests"] = n_req
+    descs["req_offset"] = req_off
+    descs["replica_offset"] = rep_off
+    trace: list[int] = []
+    n_pref = np.fromiter((len(t.prefix_suffix) for t in tmpl_of), dtype=np.int64, count=n)
+    pref_off = np.concatenate([[0], np.cumsum(n_pref)[:-1]]) if n else n_pref
+    for i, t in enumerate(tmpl_of):
+        descs[i]["trace_offset"] = len(trace)
+        trace.extend(t.trace)
+    # replicas: template rows with prefix indices made global
+    if n:
+        # gather template rows: row j of instance i = template row (tbase[which[i]] + j)
+        tsize = np.array([len(t.reps) for t in uniq], dtype=np.int64)
+        tbase = np.concatenate([[0], np.cumsum(tsize)[:-1]])
+        trows = np.zeros(int(tsize.sum()), dtype=abi.REPLICA_DESC)
+        for j, t in enumerate(uniq):
+            trows[tbase[j]: tbase[j] + tsize[j]] = t.reps
+        within = np.arange(int(n_rep.sum()), dtype=np.int64) - np.repeat(rep_off, n_rep)
+        replicas = trows[np.repeat(tbase[which], n_rep) + within]
+        shift = np.repeat(pref_off, n_rep)
+        replicas["prefix"] += shift.astype(np.int32)
+        mb = replicas["prefix_mb"] >= 0
+        replicas["prefix_mb"][mb] += shift[mb].astype(np.int32)
+    else:
+        replicas = np.zeros(0, abi.REPLICA_DESC)
+    # router-seed prefixes "{seed}:{key}:" (and ":mb") for every replica
+    texts = [f"{sp.seed}{suf}".encode("utf-8") for sp, t in zip(specs, tmpl_of)
+             for suf in t.prefix_suffix]
+    pref = np.zeros(len(texts), dtype=abi.SEED_PREFIX)
+    if texts:
+        lens = np.fromiter((len(b) for b in texts), dtype=np.int64, count=len(texts))
+        if lens.max() > abi.MAX_PREFIX_BYTES:
+            bad = texts[int(lens.argmax())].decode()
+            raise EngineCapacityError(f"router-seed prefix of {int(lens.max())} bytes exceeds "
+                                      f"{abi.MAX_PREFIX_BYTES}: {bad[:40]}...")
+        buf = b"".join(b.ljust(abi.MAX_PREFIX_BYTES, b"\0") for b in texts)
+        pref["bytes"] = np.frombuffer(buf, dtype=np.uint8).reshape(len(texts), abi.MAX_PREFIX_BYTES)
+        pref["len"] = lens
+        pref["mid_blocks"] = lens // 64
+    # request struct-of-arrays
+    cat = lambda parts, dt: np.concatenate(parts).astype(dt, copy=False) if parts else np.zeros(0, dt)  # noqa: E731
+    arrival = cat([sp.requests.arrival_ns for sp in specs], np.int64)
+    prompt = cat([sp.requests.prompt for sp in specs], np.int32)
+    output = cat([sp.requests.output for sp in specs], np.int32)
+    id_rank = cat([sp.requests.id_rank if getattr(sp.requests, "id_rank", None) is not None
+                   else _ranks_of(sp.requests.ids) for sp in specs], np.int32)
+    # est_cost (_estimate_cost) over the concatenated arrays
+    if n:
+        nz = n_req > 0
+        starts = req_off[nz]
+        out_tok = np.zeros(n, np.int64)
+        pr_tok = np.zeros(n, np.int64)
+        if len(starts):
+            out_tok[nz] = np.add.reduceat(output.astype(np.int64), starts)
+            pr_tok[nz] = np.add.reduceat(prompt.astype(np.int64), starts)
+        out_tok += n_req
+        L = descs["num_layers"].astype(np.int64)
+        work = out_tok * L
+        moe = descs["has_moe"] != 0
+        work[moe] += (out_tok + pr_tok)[moe] * L[moe] * descs["num_experts"][moe] // 4
+        descs["est_cost"] = work
     return Lowered(
         descs=descs, replicas=replicas, prefixes=pref,
         trace_counts=np.asarray(trace if trace else [0], dtype=np.int64),
-        arrival=cat(arr_parts, np.int64), prompt=cat(p_parts, np.int32),
-        output=cat(o_parts, np.int32), id_rank=cat(rank_parts, np.int32),
-        replica_keys=replica_keys, request_ids=request_ids,
+        arrival=arrival, prompt=prompt, output=output, id_rank=id_rank,
+        replica_keys=[t.keys for t in tmpl_of],
+        request_ids=[sp.requests.ids for sp in specs],
         forests=forests if forests.models else None)

@@ -79,6 +79,7 @@ class InstanceResult:
     af_micro_batches: int = 0
     event_log: np.ndarray | None = None      # fs_event_rec by seq (trace runs only)
     expert_imbalance: list[float] | None = None  # from a moe-ratio log (api.simulate)
+    per_request_values: tuple | None = None  # (ttft, tpot, e2e) lists, split_results
 
     def trace(self):
         """The reference's EventTrace of this run (needs a run with an event log)."""
@@ -122,8 +123,25 @@ class InstanceResult:
         return [self.request_ids[i] for i in order if self.completion_rank[i] >= 0]
 
 
+def _per_request_columns(low, raw) -> tuple[list, list, list]:
+    """ttft / tpot / e2e of every request of the batch as Python floats, in one
+    vectorised pass with the reference's expressions (metrics.py:91-100): exact
+    int64 ns differences, then the same IEEE divisions Python performs."""
+    arr = low.arrival
+    with np.errstate(all="ignore"):
+        ttft = (raw.first_ns - arr) / 1e9
+        e2e = (raw.done_ns - arr) / 1e9
+        n_out = low.output.astype(np.int64)
+        tpot = (e2e - ttft) / (n_out - 1)
+    tp = tpot.tolist()
+    for j in np.flatnonzero(n_out <= 1).tolist():
+        tp[j] = None
+    return ttft.tolist(), tp, e2e.tolist()
+
+
 def split_results(low, raw, modes: list[str]) -> list[InstanceResult]:
     out = []
+    cols = _per_request_columns(low, raw) if low.n_requests else ([], [], [])
     for i in range(low.n_instances):
         d = low.descs[i]
         o, n = int(d["req_offset"]), int(d["n_requests"])
@@ -137,7 +155,8 @@ def split_results(low, raw, modes: list[str]) -> list[InstanceResult]:
             total_gpus=int(d["total_gpus"]), mode=modes[i],
             pool_capacity=low.replicas["kv_pool_tokens"][ro:ro + nr].tolist(),
             has_moe=bool(d["has_moe"]), kv_bytes_per_token=int(d["kv_bytes_per_token"]),
-            af_micro_batches=int(d["af_micro_batches"]))
+            af_micro_batches=int(d["af_micro_batches"]),
+            per_request_values=(cols[0][o:o + n], cols[1][o:o + n], cols[2][o:o + n]))
         if raw.log is not None:
             if raw.log.spec.batch_cap:
                 res.batches = raw.log.instance_batches(i)
@@ -173,15 +192,20 @@ def compute_metrics(result, deployment=None) -> MetricsBundle:
     if not result.ok:
         raise IncompleteTrace(str(result.error()))
     row = result.row
-    per_request = {}
-    for i, rid in enumerate(result.request_ids):
-        arr = int(result.arrival_ns[i])
-        ttft = (int(result.first_token_ns[i]) - arr) / 1e9
-        e2e = (int(result.done_ns[i]) - arr) / 1e9
-        n_out = int(result.output[i])
-        per_request[rid] = {"ttft_s": ttft,
-                            "tpot_s": (e2e - ttft) / (n_out - 1) if n_out > 1 else None,
-                            "e2e_s": e2e}
+    pv = getattr(result, "per_request_values", None)
+    if pv is not None:
+        per_request = {rid: {"ttft_s": a, "tpot_s": b, "e2e_s": c}
+                       for rid, a, b, c in zip(result.request_ids, *pv)}
+    else:
+        per_request = {}
+        for i, rid in enumerate(result.request_ids):
+            arr = int(result.arrival_ns[i])
+            ttft = (int(result.first_token_ns[i]) - arr) / 1e9
+            e2e = (int(result.done_ns[i]) - arr) / 1e9
+            n_out = int(result.output[i])
+            per_request[rid] = {"ttft_s": ttft,
+                                "tpot_s": (e2e - ttft) / (n_out - 1) if n_out > 1 else None,
+                                "e2e_s": e2e}
     busy = {}
     for k, o in zip(result.replica_keys, result.replica_out):
         if int(o["steps_executed"]) > 0:
