@@ -897,6 +897,87 @@ __device__ __noinline__ int learned_moe_layer_warp(const EngineParams& P, Inst& 
 #define FFN_DENSE_US(c, n) dense_ffn_us(d, (c), (n))
 #endif
 
+// The per-batch operator costs that do not vary by layer, one per lane, then
+// broadcast: lane 0 qkv_proj_us, 1 attention_us, 2 out_proj_us, 3 the dense ffn
+// (grouped GEMM of one local expert), 4 tp_collective_us, 5 the (pp - 1) stage
+// transfers. Each lane runs the same fp64 operations, in the same order, as the
+// serial helpers above (qkv_us, attn_cost_us, ...), so every value is bit-identical;
+// the warp pays for one roofline's two divisions instead of six.
+struct BatchTerms {
+  double qkv, att, out, ffn, coll, pp;
+};
+__device__ __forceinline__ BatchTerms batch_terms(const fs_instance_desc* d, const fs_cost_ctx& c,
+                                                  const BatchShape& b, int lane) {
+  int hq, hkv;
+  heads_of(d, c.tp, hq, hkv);
+  const int64_t n = b.n_tokens, dt = d->dtype_bytes, hd = d->head_dim, dm = d->d_model;
+  const int j = lane < 6 ? lane : 5;
+  // numerators / denominators of the lane's two divisions
+  double num1, den1, num2, den2;
+  if (j == 0 || j == 2 || j == 3) {  // linear_us / grouped_gemm_us rooflines
+    int64_t a, bb, cc, e;
+    int64_t nbytes;
+    if (j == 3) {  // dense FFN: routed n, one active expert, d_ff / tp (>= 1)
+      int64_t dff = d->d_ff / c.tp;
+      if (dff < 1) dff = 1;
+      const int64_t nm = d->ffn_matrices;
+      a = nm; bb = n; cc = dm; e = dff;
+      nbytes = 1 * nm * dm * dff * dt + n * nm * (dm + dff) * dt;
+    } else {       // linear(m = n, nn, k)
+      const int64_t nn = j == 0 ? (int64_t)(hq + 2 * hkv) * hd : dm;
+      const int64_t k = j == 0 ? dm : (int64_t)hq * hd;
+      a = n; bb = nn; cc = k; e = 1;
+      nbytes = dt * (n * nn + nn * k + n * k);
+    }
+    double f = 2.0 * i2d(a);
+    f = f * i2d(bb);
+    f = f * i2d(cc);
+    if (j == 3) f = f * i2d(e);
+    num1 = f; den1 = c.peak_flops;
+    num2 = i2d(nbytes); den2 = c.mem_bw;
+  } else if (j == 1) {  // attention_us_from
+    double kvb = 2.0 * i2d(b.sum_kv);
+    kvb = kvb * (double)hkv;
+    kvb = kvb * (double)hd;
+    kvb = kvb * (double)dt;
+    double qob = 2.0 * i2d(b.sum_q);
+    qob = qob * (double)hq;
+    qob = qob * (double)hd;
+    qob = qob * (double)dt;
+    num1 = b.attn_flops; den1 = c.peak_flops;
+    num2 = kvb + qob; den2 = c.mem_bw;
+  } else if (j == 4) {  // tpcoll_us: collective_int(all_reduce, n d_model dt, tp)
+    num1 = i2d(n * dm * dt * (int64_t)(c.tp - 1)); den1 = (double)c.tp;
+    num2 = 0.0; den2 = 1.0;
+  } else {  // pp transfer: intra latency + n d_model dt / bandwidth
+    num1 = 0.0; den1 = 1.0;
+    num2 = i2d(n * dm * dt); den2 = d->intra_bandwidth_bps;
+  }
+  const double q1 = num1 / den1, q2 = num2 / den2;
+  double v;
+  if (j <= 3) {
+    v = c.kernel_overhead_us + py_max(q1, q2) * 1e6;
+  } else if (j == 4) {
+    if (c.tp == 1) {
+      v = 0.0;
+    } else {
+      const double wire = q1 / d->intra_bandwidth_bps;
+      v = (2.0 * d->intra_latency_s + 2.0 * wire) * 1e6;
+    }
+  } else {
+    const double tt = d->intra_latency_s + q2;
+    v = (double)(c.pp - 1) * (tt * 1e6);
+  }
+  BatchTerms t;
+  t.qkv = __shfl_sync(FS_FULL, v, 0);
+  t.att = __shfl_sync(FS_FULL, v, 1);
+  t.out = __shfl_sync(FS_FULL, v, 2);
+  t.ffn = __shfl_sync(FS_FULL, v, 3);
+  t.coll = __shfl_sync(FS_FULL, v, 4);
+  t.pp = __shfl_sync(FS_FULL, v, 5);
+  return t;
+}
+
 // Duration in us (same on all lanes). moe_out (global) receives the per-layer
 // moe_imbalance values round(expert / mean(per_rank), 6) when non-null.
 __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
@@ -906,25 +987,32 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
   const fs_cost_ctx c = rd.cost;
   const int L = d->num_layers;
   const int64_t n = b.n_tokens;
-  const double qkv = qkv_us(d, c, n);
+  const BatchTerms bt = batch_terms(d, c, b, I.lane);
+  const double qkv = bt.qkv, out = bt.out, coll = bt.coll;
 #if FS_LEARNED
-  const double att = isnan(b.learned_attn) ? attn_cost_us(d, c, b.attn_flops, b.sum_q, b.sum_kv)
-                                           : b.learned_attn;
+  const double att = isnan(b.learned_attn) ? bt.att : b.learned_attn;
 #else
-  const double att = attn_cost_us(d, c, b.attn_flops, b.sum_q, b.sum_kv);
+  const double att = bt.att;
 #endif
-  const double out = out_us(d, c, n);
-  const double coll = tpcoll_us(d, c, n);
   PySum ls;
   ls.init();
   if (FS_DENSE_ONLY || !d->has_moe) {
-    const double ffn = FFN_DENSE_US(c, n);
+#if FS_LEARNED
+    const double ffn = d->gg_forest != -1 ? learned_dense_ffn_us(P, I, c, n, sm) : bt.ffn;
+#else
+    const double ffn = bt.ffn;
+#endif
     double tot = qkv + att;
     tot = tot + out;
     tot = tot + coll;
     tot = tot + ffn;
     tot = tot + coll;
-    for (int l = 0; l < L; l++) ls.add(tot);  // never L * tot: Python adds layer by layer
+    // sum(layer.total_us for L identical layers) (cluster.py:345): CPython's
+    // Neumaier sum of L copies of tot is exactly fl(L * tot) -- every step's error
+    // is caught exactly in the compensation, a multiple of ulp(tot) below 2^53 ulp
+    // for L < 2^26 -- so one rounded product replaces the L-step chain
+    // (tests/test_known_answers.py pins it against Python's sum()).
+    return __dmul_rn((double)L, tot) + bt.pp;
   } else {
     const bool board = use_job_board(I.d, d->routing_policy, n);
     const bool log_routes = P.log_enabled && P.log.routes;
@@ -983,10 +1071,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
       }
     }
   }
-  const int64_t bytes = n * (int64_t)d->d_model * d->dtype_bytes;
-  const double tt = d->intra_latency_s + i2d(bytes) / d->intra_bandwidth_bps;
-  const double pp = (double)(c.pp - 1) * (tt * 1e6);
-  return ls.result() + pp;
+  return ls.result() + bt.pp;
 }
 
 // ---- optional event trace (fs_event_rec at index seq; one lane writes) ------------------

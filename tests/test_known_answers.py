@@ -63,3 +63,19 @@ def test_invalid_topk_and_alpha_on_device(engine):
     assert st.tolist() == [8]  # FS_ERR_INVALID_TOPK (routing.py:76-77)
     _, st = engine.route_tokens([10], [1], 8, 2, "dirichlet_skew", 0.0)
     assert st.tolist() == [5]  # RoutingError: dirichlet_skew needs alpha > 0
+
+
+def test_python_sum_of_identical_layers_is_one_rounded_product():
+    """execute_batch (csrc/fs_sim.cuh) replaces the L-step Neumaier sum of L
+    identical layer totals (cluster.py:345) by fl(L * x). CPython's sum() catches
+    every step's rounding error exactly in its compensation (a multiple of ulp(x)
+    below 2^53 ulp for L < 2^26), so the two are the same double."""
+    import math
+    import random
+    rng = random.Random(2508)
+    xs = [0.1, 1 / 3, 2 / 3, 0.30000000000000004, 123456.789, 5e-324 * 12345]
+    xs += [rng.lognormvariate(5, 4) for _ in range(3000)]
+    xs += [math.ldexp(rng.random() + 0.5, rng.randint(-60, 60)) for _ in range(3000)]
+    for x in xs:
+        for L in (1, 2, 3, 7, 32, 61, 80, 127, 128, rng.randint(1, 5000)):
+            assert sum([x] * L) == L * x, (x, L)
