@@ -47,7 +47,7 @@ extern "C" {
 #define FS_MAX_EXPERTS 1024       /* experts per MoE layer                              */
 #define FS_MAX_TOPK 16            /* top_k for uniform routing                         */
 #define FS_MAX_MICRO_BATCHES 64   /* AF micro-batches per step                         */
-#define FS_MAX_REPLICAS 64        /* replicas per instance                             */
+#define FS_MAX_REPLICAS 65536     /* replicas per instance (state spills to HBM)       */
 
 enum fs_mode { FS_MODE_COLOCATED = 0, FS_MODE_PD = 1, FS_MODE_AF = 2 };
 
@@ -100,10 +100,15 @@ typedef struct {
   int32_t tp, ep, moe_tp, pp;
 } fs_cost_ctx;                /* 40 bytes */
 
-/* Router-seed prefix (base.py:63-65): bytes = "{master_seed}:{scope}:" for a
+/* Router-seed prefix (base.py:63-65): the text "{master_seed}:{scope}:" for a
  * replica scope or "{master_seed}:{replica_key}:mb" for an AF micro-batch scope
- * (af.py:317). mid[] is the SHA-256 state after the first mid_blocks complete
- * 64-byte blocks of bytes[], so the device only hashes the tail. */
+ * (af.py:317), len bytes long, mid_blocks = len / 64.
+ *  - len <= FS_MAX_PREFIX_BYTES: bytes[] holds the whole text; the engine computes
+ *    the SHA-256 state after its first mid_blocks complete 64-byte blocks.
+ *  - longer (no limit): bytes[] holds only the last len - 64 * mid_blocks (< 64)
+ *    bytes and mid[] the SHA-256 state after the first mid_blocks blocks, computed
+ *    by the caller.
+ * Either way the device hashes only the tail and the step/layer digits. */
 typedef struct {
   uint8_t bytes[FS_MAX_PREFIX_BYTES];
   int32_t len;

@@ -72,10 +72,12 @@ static void sha256_block(uint32_t h[8], const uint8_t* p) {
   h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
 }
 
-/* First 4 digest bytes, big-endian, of sha256(msg): int.from_bytes(digest[:4], "big"). */
-static uint32_t sha256_first_word(const uint8_t* msg, size_t len) {
-  uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
-                   0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+/* First 4 digest bytes, big-endian, of sha256(prior ++ msg) where h0 is the state
+ * after the prior_bytes (a multiple of 64) of prior: int.from_bytes(digest[:4], "big"). */
+static uint32_t sha256_first_word_from(const uint32_t h0[8], uint64_t prior_bytes,
+                                       const uint8_t* msg, size_t len) {
+  uint32_t h[8];
+  memcpy(h, h0, sizeof h);
   size_t off = 0;
   while (len - off >= 64) { sha256_block(h, msg + off); off += 64; }
   uint8_t blk[128];
@@ -84,20 +86,31 @@ static uint32_t sha256_first_word(const uint8_t* msg, size_t len) {
   memcpy(blk, msg + off, rem);
   blk[rem] = 0x80;
   size_t nblk = (rem + 9 <= 64) ? 1 : 2;
-  uint64_t bits = (uint64_t)len * 8u;
+  uint64_t bits = (prior_bytes + (uint64_t)len) * 8u;
   for (int i = 0; i < 8; i++) blk[nblk * 64 - 1 - i] = (uint8_t)(bits >> (8 * i));
   for (size_t b = 0; b < nblk; b++) sha256_block(h, blk + 64 * b);
   return h[0];
+}
+static const uint32_t SHA256_IV[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                                      0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+static uint32_t sha256_first_word(const uint8_t* msg, size_t len) {
+  return sha256_first_word_from(SHA256_IV, 0, msg, len);
 }
 
 /* derive_router_seed(master, scope, step, layer): prefix holds "{master}:{scope}:"
  * (or "{master}:{key}:mb" with the micro-batch index as the first tail integer). */
 static uint32_t router_seed(const fs_seed_prefix* pf, int mb, int64_t step, int32_t layer) {
   char buf[FS_MAX_PREFIX_BYTES + 64];
-  memcpy(buf, pf->bytes, (size_t)pf->len);
-  int n = pf->len;
+  /* a prefix longer than bytes[] arrives as its tail plus the SHA-256 state of
+   * its leading 64-byte blocks (include/frontier_b200.h, fs_seed_prefix) */
+  const int lng = pf->len > FS_MAX_PREFIX_BYTES;
+  const int n0 = lng ? pf->len - 64 * pf->mid_blocks : pf->len;
+  memcpy(buf, pf->bytes, (size_t)n0);
+  int n = n0;
   if (mb > 0) n += sprintf(buf + n, "%d:", mb);
   n += sprintf(buf + n, "%lld:%d", (long long)step, (int)layer);
+  if (lng) return sha256_first_word_from(pf->mid, 64u * (uint64_t)pf->mid_blocks,
+                                         (const uint8_t*)buf, (size_t)n);
   return sha256_first_word((const uint8_t*)buf, (size_t)n);
 }
 
@@ -1742,7 +1755,8 @@ static void* worker(void* arg) {
     int64_t* fn = j->pr.first_token_ns ? j->pr.first_token_ns + o : (int64_t*)malloc(8 * (size_t)(N + 1));
     int64_t* dn = j->pr.done_ns ? j->pr.done_ns + o : (int64_t*)malloc(8 * (size_t)(N + 1));
     int32_t* dr = j->pr.completion_rank ? j->pr.completion_rank + o : (int32_t*)malloc(4 * (size_t)(N + 1));
-    fs_replica_out tmp[FS_MAX_REPLICAS];
+    fs_replica_out* tmp = j->ro ? NULL : (fs_replica_out*)malloc(sizeof(fs_replica_out) *
+                                                                  (size_t)(d->n_replicas + 1));
     fs_replica_out* ro = j->ro ? j->ro + d->replica_offset : tmp;
     fso_run_instance(d, j->reps + d->replica_offset, j->pf, j->tc, j->rq.arrival_ns + o,
                      j->rq.prompt_tokens + o, j->rq.output_tokens + o, j->rq.id_rank + o,
@@ -1750,6 +1764,7 @@ static void* worker(void* arg) {
     if (!j->pr.first_token_ns) free(fn);
     if (!j->pr.done_ns) free(dn);
     if (!j->pr.completion_rank) free(dr);
+    free(tmp);
   }
   return NULL;
 }

@@ -14,7 +14,7 @@ MAX_PREFIX_BYTES = 192
 MAX_EXPERTS = 1024
 MAX_TOPK = 16
 MAX_MICRO_BATCHES = 64
-MAX_REPLICAS = 64
+MAX_REPLICAS = 65536
 MAX_FOREST_TREES = 256  # fs_forest.cuh kMaxForestTrees (per-warp leaf sort in shared memory)
 DEFAULT_MAX_EVENTS = 50_000_000
 

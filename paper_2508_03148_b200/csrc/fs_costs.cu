@@ -797,7 +797,9 @@ __global__ void seeds_kernel(const fs_seed_prefix* pf, const uint32_t* mid, cons
   if (mb[i] > 0) ints[k++] = mb[i];
   ints[k++] = steps[i];
   ints[k++] = layers[i];
-  out[i] = sha256_tail_first_word(mid + (int64_t)pidx[i] * 8, p->len / 64, p->bytes, p->len, ints, k);
+  int tl;
+  const uint8_t* tail = prefix_tail(p, tl);
+  out[i] = sha256_tail_first_word(mid + (int64_t)pidx[i] * 8, p->mid_blocks, tail, tl, ints, k);
 }
 
 // fs_eval (diagnostics): the pure functions the simulator composes, one record

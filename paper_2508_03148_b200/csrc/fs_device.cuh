@@ -188,18 +188,26 @@ __device__ inline void sha256_compress(uint32_t h[8], const uint32_t wblk[16]) {
   h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
 }
 
-// Message = prefix[mid_blocks*64 .. len) ++ ascii(ints joined by ':'), hashed from
-// the midstate `mid` (state after the first mid_blocks full blocks of the prefix).
-// Returns int.from_bytes(sha256(msg)[:4], "big").
+// A prefix's bytes after its first mid_blocks full 64-byte blocks (include/
+// frontier_b200.h: a long prefix stores only those, its midstate comes from the host).
+__device__ __forceinline__ const uint8_t* prefix_tail(const fs_seed_prefix* pf, int& tail_len) {
+  const int skip = pf->mid_blocks * 64;
+  tail_len = pf->len - skip;
+  return pf->len > FS_MAX_PREFIX_BYTES ? pf->bytes : pf->bytes + skip;
+}
+
+// Message = prefix ++ ascii(ints joined by ':'), hashed from the midstate `mid`
+// (state after the first mid_blocks full blocks of the prefix); `tail` holds the
+// prefix's remaining tail_len bytes. Returns int.from_bytes(sha256(msg)[:4], "big").
 __device__ inline uint32_t sha256_tail_first_word(const uint32_t mid[8], int mid_blocks,
-                                                  const uint8_t* prefix, int plen,
+                                                  const uint8_t* tail, int tail_len,
                                                   const int64_t* ints, int nints) {
   uint32_t wbuf[32];  // up to two 64-byte blocks
 #pragma unroll
   for (int i = 0; i < 32; i++) wbuf[i] = 0;
   int pos = 0;
-  for (int i = mid_blocks * 64; i < plen; i++, pos++)
-    wbuf[pos >> 2] |= (uint32_t)prefix[i] << (24 - 8 * (pos & 3));
+  for (int i = 0; i < tail_len; i++, pos++)
+    wbuf[pos >> 2] |= (uint32_t)tail[i] << (24 - 8 * (pos & 3));
   for (int j = 0; j < nints; j++) {
     if (j) { wbuf[pos >> 2] |= (uint32_t)':' << (24 - 8 * (pos & 3)); pos++; }
     int64_t v = ints[j];

@@ -13,7 +13,11 @@ __global__ void midstate_kernel(const fs_seed_prefix* pf, uint32_t* mid, int n) 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t h[8];
-  sha256_midstate(pf[i].bytes, pf[i].len / 64, h);
+  if (pf[i].len > FS_MAX_PREFIX_BYTES) {  // long prefix: the host hashed its leading blocks
+    for (int k = 0; k < 8; k++) h[k] = pf[i].mid[k];
+  } else {
+    sha256_midstate(pf[i].bytes, pf[i].mid_blocks, h);
+  }
   for (int k = 0; k < 8; k++) mid[(int64_t)i * 8 + k] = h[k];
 }
 

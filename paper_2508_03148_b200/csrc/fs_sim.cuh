@@ -238,8 +238,10 @@ __device__ void derive_layer_keys(const EngineParams& P, const Inst& I, int pref
     if (mb > 0) ints[n++] = mb;
     ints[n++] = step;
     ints[n++] = layer;
-    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->len / 64,
-                                                 pf->bytes, pf->len, ints, n);
+    int tl;
+    const uint8_t* tail = prefix_tail(pf, tl);
+    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->mid_blocks,
+                                                 tail, tl, ints, n);
     uint64_t key[2];
     routing_key((uint64_t)seed, key);
     sm->keys[I.lane][0] = key[0];
@@ -620,8 +622,10 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
     if (mb > 0) ints[n++] = mb;
     ints[n++] = step;
     ints[n++] = layer;
-    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->len / 64,
-                                                 pf->bytes, pf->len, ints, n);
+    int tl;
+    const uint8_t* tail = prefix_tail(pf, tl);
+    const uint32_t seed = sha256_tail_first_word(P.midstate + (int64_t)prefix * 8, pf->mid_blocks,
+                                                 tail, tl, ints, n);
     uint64_t key[2];
     routing_key((uint64_t)seed, key);
     job->keys[I.lane][0] = key[0];

@@ -73,15 +73,62 @@ def _cost(hw, tp, ep, moe_tp, pp) -> tuple:
             int(tp), int(ep), int(moe_tp), int(pp))
 
 
-def _prefix(text: str) -> np.void:
-    b = text.encode("utf-8")
-    if len(b) > abi.MAX_PREFIX_BYTES:
-        raise EngineCapacityError(
-            f"router-seed prefix of {len(b)} bytes exceeds {abi.MAX_PREFIX_BYTES}: {text[:40]}...")
-    rec = np.zeros((), dtype=abi.SEED_PREFIX)
-    rec["bytes"][: len(b)] = np.frombuffer(b, dtype=np.uint8)
+_SHA256_K = (
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2)
+_SHA256_IV = (0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+              0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19)
+
+
+def sha256_midstate(data: bytes) -> tuple[int, ...]:
+    """SHA-256 state after compressing the complete 64-byte blocks of `data` (FIPS
+    180-4 compression function; hashlib does not expose midstates)."""
+    m32 = 0xFFFFFFFF
+
+    def rotr(x: int, n: int) -> int:
+        return ((x >> n) | (x << (32 - n))) & m32
+
+    h = list(_SHA256_IV)
+    for b in range(len(data) // 64):
+        w = list(int.from_bytes(data[64 * b + 4 * i: 64 * b + 4 * i + 4], "big") for i in range(16))
+        for i in range(16, 64):
+            s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3)
+            s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10)
+            w.append((w[i - 16] + s0 + w[i - 7] + s1) & m32)
+        a, bb, c, d, e, f, g, hh = h
+        for i in range(64):
+            t1 = (hh + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g))
+                  + _SHA256_K[i] + w[i]) & m32
+            t2 = ((rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & bb) ^ (a & c) ^ (bb & c))) & m32
+            hh, g, f, e, d, c, bb, a = g, f, e, (d + t1) & m32, c, bb, a, (t1 + t2) & m32
+        h = [(x + y) & m32 for x, y in zip(h, (a, bb, c, d, e, f, g, hh))]
+    return tuple(h)
+
+
+def _fill_prefix(rec, b: bytes) -> None:
+    """fs_seed_prefix for the text `b` (include/frontier_b200.h): short texts whole,
+    long ones as their tail and the midstate of their leading 64-byte blocks."""
     rec["len"] = len(b)
     rec["mid_blocks"] = len(b) // 64
+    if len(b) <= abi.MAX_PREFIX_BYTES:
+        rec["bytes"][: len(b)] = np.frombuffer(b, dtype=np.uint8)
+        return
+    skip = 64 * (len(b) // 64)
+    tail = b[skip:]
+    if tail:
+        rec["bytes"][: len(tail)] = np.frombuffer(tail, dtype=np.uint8)
+    rec["mid"] = sha256_midstate(b[:skip])
+
+
+def _prefix(text: str) -> np.void:
+    rec = np.zeros((), dtype=abi.SEED_PREFIX)
+    _fill_prefix(rec, text.encode("utf-8"))
     return rec
 
 
@@ -175,9 +222,6 @@ def check_spec(sp: InstanceSpec) -> None:
     ids = sp.requests.ids
     if ids is not _RANKS_CACHE.get(len(ids), (None,))[0] and len(set(ids)) != len(ids):
         raise SimulationError("duplicate request id")
-    plen = len(str(sp.seed)) + hit[2] + 4  # "{seed}:{key}:mb"
-    if plen > abi.MAX_PREFIX_BYTES:
-        _prefix(f"{sp.seed}:{'x' * hit[2]}:mb")  # raises with the reference-style message
     sp.__dict__["_checked"] = True
 
 
@@ -352,14 +396,18 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
     pref = np.zeros(len(texts), dtype=abi.SEED_PREFIX)
     if texts:
         lens = np.fromiter((len(b) for b in texts), dtype=np.int64, count=len(texts))
-        if lens.max() > abi.MAX_PREFIX_BYTES:
-            bad = texts[int(lens.argmax())].decode()
-            raise EngineCapacityError(f"router-seed prefix of {int(lens.max())} bytes exceeds "
-                                      f"{abi.MAX_PREFIX_BYTES}: {bad[:40]}...")
+        long_ = np.flatnonzero(lens > abi.MAX_PREFIX_BYTES).tolist()
+        for j in long_:  # tail + host midstate (rare: cluster ids of ~180+ characters)
+            texts[j] = b""
         buf = b"".join(b.ljust(abi.MAX_PREFIX_BYTES, b"\0") for b in texts)
         pref["bytes"] = np.frombuffer(buf, dtype=np.uint8).reshape(len(texts), abi.MAX_PREFIX_BYTES)
         pref["len"] = lens
         pref["mid_blocks"] = lens // 64
+        if long_:
+            full = [f"{sp.seed}{suf}".encode("utf-8") for sp, t in zip(specs, tmpl_of)
+                    for suf in t.prefix_suffix]
+            for j in long_:
+                _fill_prefix(pref[j], full[j])
     # request struct-of-arrays
     cat = lambda parts, dt: np.concatenate(parts).astype(dt, copy=False) if parts else np.zeros(0, dt)  # noqa: E731
     arrival = cat([sp.requests.arrival_ns for sp in specs], np.int64)

@@ -594,6 +594,35 @@ def dirichlet_fixtures() -> dict:
     return out
 
 
+def capacity_scenarios() -> dict[str, dict]:
+    """Past the round-1 engine limits: > 64 replicas per instance (PD with many
+    prefill and decode replicas, co-located MoE), and cluster ids long enough that
+    the router-seed prefix "{seed}:{id}/{i}:mb" exceeds 192 bytes."""
+    from paper_2508_03148_b200 import workloads as W
+    out = {}
+    d = W.c3_pd(160, seed=3, tight=True)
+    d["clusters"][0]["num_replicas"] = 40
+    d["clusters"][1]["num_replicas"] = 60
+    d["workload"]["arrival"]["rate_rps"] = 200.0
+    out["pd_40x60_replicas"] = d
+    d = W.c5_sweep_configs(8)[48 + 5]  # Mixtral co-located EP, 8 requests per seed
+    d = copy.deepcopy(d)
+    d["clusters"][0]["num_replicas"] = 80
+    d["workload"]["num_requests"] = 120
+    d["workload"]["arrival"]["rate_rps"] = 400.0
+    d["seed"] = 11
+    out["moe_colocated_80_replicas"] = d
+    d = W.c3_pd(40, seed=5, tight=False)
+    d["clusters"][0]["id"] = "prefill-" + "p" * 230
+    d["clusters"][1]["id"] = "decode-" + "d" * 300
+    d["clusters"][1]["num_replicas"] = 3
+    out["pd_long_cluster_ids"] = d
+    d = W.c4_af(12, seed=9)
+    d["clusters"][0]["id"] = "attention-" + "a" * 260
+    out["af_long_cluster_id"] = d
+    return out
+
+
 def write(name: str, payload) -> None:
     payload = {"numpy": np.__version__, "python": sys.version.split()[0], "data": payload}
     path = os.path.join(HERE, f"{name}.json.gz")
@@ -620,6 +649,14 @@ def main() -> None:
             print(name, sc[name].get("iterations"), sc[name].get("error"),
                   f"{sc[name]['wall_s']:.2f}s")
         write("scenarios", sc)
+    if only is not None and "capacity" in only:
+        cap = {}
+        for name, doc in capacity_scenarios().items():
+            moe = "moe" in doc["model"]
+            cap[name] = record(doc, with_batches=True, with_routes=moe and name.startswith("af"))
+            print(name, cap[name].get("iterations"), cap[name].get("error"),
+                  f"{cap[name]['wall_s']:.2f}s")
+        write("capacity", cap)
     if only is None or "learned_moe" in only:
         write("learned_moe", learned_moe_fixtures())
     if only is None or "dirichlet" in only:
