@@ -64,9 +64,13 @@ struct fs_engine {
   int64_t forest_gen = 0;         // bumped by every fs_set_forests
   int64_t staged_forest_gen = -1; // forest_gen the staged batch's indices refer to
   bool staged_uses_forests = false;
-  bool learned = false;  // staged batch uses the learned simulation variant
-  int variant = 0;       // fs::SimVariant of the staged batch
+  bool learned = false;  // staged batch has instances for the learned simulation variant
+  int variant = 0;       // fs::SimVariant of the first wave (single-wave batches: the batch)
   int n_moe = 0;         // MoE instances of the staged batch (first in the order)
+  // waves: instances bucketed by kernel variant, consecutive in the order array
+  struct Wave { int variant, start, count, slots; };
+  Wave waves[4];
+  int n_waves = 0;
   int split_families = 1;  // FS_SPLIT_FAMILIES: MoE and dense instances in separate waves
   int dense_variant = 1;   // FS_DENSE_VARIANT: dense instances on the MoE-free kernel
   // routing job geometry (environment knobs read at fs_create)
@@ -198,15 +202,51 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
       af_base[i] = -1;
     }
   }
-  // longest estimated cost first (the work queue is consumed in this order)
+  // Kernel variant per instance: learned models / dirichlet_skew need the extended
+  // kernel, long MoE rows (>= 64 experts) the long-row one, other MoE instances the
+  // sweep kernel, dense ones the MoE-free kernel. Each variant's instances form one
+  // wave (fs_launch_async), so one learned or DeepSeek-V3 instance no longer moves
+  // the whole batch onto a slower kernel; within a wave, longest estimated cost first
+  // (the work queue is consumed in this order).
+  const bool no_longrow = getenv("FS_NO_LONGROW") != nullptr;
+  const bool split = e->split_families != 0;
+  std::vector<int> cls(n_instances);
+  for (int i = 0; i < n_instances; i++) {
+    const fs_instance_desc& d = descs[i];
+    const bool lrn = d.attn_forest != -1 || d.gg_forest != -1 ||
+                     (d.has_moe && d.routing_policy == FS_ROUTE_DIRICHLET);
+    int c;
+    if (lrn) c = fs::kSimLearned;
+    else if (d.has_moe && d.num_experts >= 64 && !no_longrow) c = fs::kSimLongRow;
+    else if (d.has_moe || !e->dense_variant) c = fs::kSimAnalytic;
+    else c = fs::kSimDense;
+    cls[i] = c;
+  }
+  if (!split) {  // FS_SPLIT_FAMILIES=0: one wave on the most general variant present
+    int v = fs::kSimDense;
+    for (int i = 0; i < n_instances; i++) {
+      if (cls[i] == fs::kSimLearned) v = fs::kSimLearned;
+      else if (cls[i] == fs::kSimLongRow && v != fs::kSimLearned) v = fs::kSimLongRow;
+      else if (cls[i] == fs::kSimAnalytic && v == fs::kSimDense) v = fs::kSimAnalytic;
+    }
+    for (int i = 0; i < n_instances; i++) cls[i] = v;
+  }
+  static const int kWaveOrder[4] = {fs::kSimLearned, fs::kSimLongRow, fs::kSimAnalytic,
+                                    fs::kSimDense};
+  auto rank_of = [&](int c) { for (int k = 0; k < 4; k++) if (kWaveOrder[k] == c) return k; return 4; };
   std::vector<int32_t> order(n_instances);
   std::iota(order.begin(), order.end(), 0);
-  // MoE instances first, then the dense ones; each group longest estimated cost
-  // first. fs_launch_async runs the two groups as separate waves (see there).
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    if (descs[a].has_moe != descs[b].has_moe) return descs[a].has_moe > descs[b].has_moe;
+    if (cls[a] != cls[b]) return rank_of(cls[a]) < rank_of(cls[b]);
     return descs[a].est_cost > descs[b].est_cost;
   });
+  e->n_waves = 0;
+  for (int k = 0; k < n_instances;) {
+    int j = k;
+    while (j < n_instances && cls[order[j]] == cls[order[k]]) j++;
+    e->waves[e->n_waves++] = {cls[order[k]], k, j - k, 0};
+    k = j;
+  }
   e->n_moe = 0;
   for (int i = 0; i < n_instances; i++) e->n_moe += descs[i].has_moe ? 1 : 0;
 
@@ -294,14 +334,19 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   int max_e = 0;
   for (int i = 0; i < n_instances; i++)
     if (descs[i].has_moe) max_e = std::max(max_e, descs[i].num_experts);
-  // kernel variant: learned models / dirichlet need the extended kernel; long MoE
-  // rows (>= 64 experts) the long-row one; everything else the sweep kernel
-  e->variant = e->learned ? fs::kSimLearned
-                          : (max_e >= 64 && !getenv("FS_NO_LONGROW") ? fs::kSimLongRow
-                                                                      : fs::kSimAnalytic);
-  if (e->variant == fs::kSimAnalytic && max_e == 0 && e->dense_variant) e->variant = fs::kSimDense;
-  // MoE batches launch the full wave: warps without an instance help route
-  P.n_slots = fs::simulation_slots(e->n_sms, n_instances, e->variant, e->sim_ctas, max_e > 0);
+  e->variant = e->n_waves ? e->waves[0].variant : fs::kSimAnalytic;
+  // per-wave resident grid; waves with MoE instances launch the full wave so warps
+  // without an instance help route. Job-board slots cover the largest wave.
+  P.n_slots = 0;
+  for (int w = 0; w < e->n_waves; w++) {
+    bool moe = false;
+    for (int k = e->waves[w].start; k < e->waves[w].start + e->waves[w].count; k++)
+      moe |= descs[order[k]].has_moe != 0;
+    e->waves[w].slots = fs::simulation_slots(e->n_sms, e->waves[w].count, e->waves[w].variant,
+                                             e->sim_ctas, moe);
+    P.n_slots = std::max(P.n_slots, e->waves[w].slots);
+  }
+  if (P.n_slots == 0) P.n_slots = 32;
   P.chunk_blocks = e->chunk_blocks;
   P.job_max_e = std::min(max_e, FS_MAX_EXPERTS);
   FS_CHECK(e->inst_done.ensure(2 * sizeof(int32_t)));
@@ -352,25 +397,19 @@ int fs_launch_async(fs_engine* e, void* stream) {
   if (e->params.jobs)
     FS_CHECK(cudaMemsetAsync(e->jobs.p, 0, (size_t)e->params.n_slots * sizeof(fs::RouteJob), s));
   e->last_launches = 0;
-  const int n = e->params.n_inst, nm = e->n_moe;
-  if (e->split_families && nm > 0 && nm < n) {
-    // Two waves: the MoE instances (routing-heavy code) then the dense ones. Mixed
-    // on the same SMs the two code paths fight over instruction fetch: the C5 sweep
-    // takes 280 ms mixed, 184 + 71 ms as separate waves.
-    fs::EngineParams moe = e->params, dense = e->params;
-    moe.n_inst = nm;
-    dense.n_inst = n - nm;
-    dense.order = e->params.order + nm;
-    e->last_launches += fs::launch_simulation(moe, e->variant, s);
-    FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
-    FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
-    const int dv = (e->variant != fs::kSimLearned && e->dense_variant) ? fs::kSimDense : e->variant;
-    if (dv == fs::kSimDense)  // its own resident wave (slots only index routing jobs,
-                              // which the dense variant has none of)
-      dense.n_slots = fs::simulation_slots(e->n_sms, n - nm, dv, e->sim_ctas, false);
-    e->last_launches += fs::launch_simulation(dense, dv, s);
-  } else {
-    e->last_launches += fs::launch_simulation(e->params, e->variant, s);
+  // One wave per kernel variant, back to back on the stream: different variants on
+  // the same SMs fight over instruction fetch (the C5 sweep took 280 ms with its MoE
+  // and dense instances mixed, 184 + 71 ms as separate waves).
+  for (int w = 0; w < e->n_waves; w++) {
+    fs::EngineParams p = e->params;
+    p.n_inst = e->waves[w].count;
+    p.order = e->params.order + e->waves[w].start;
+    p.n_slots = e->waves[w].slots;
+    if (w > 0) {
+      FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
+      FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
+    }
+    e->last_launches += fs::launch_simulation(p, e->waves[w].variant, s);
   }
   e->last_launches += fs::launch_metrics(e->params, s);
   FS_CHECK(cudaGetLastError());

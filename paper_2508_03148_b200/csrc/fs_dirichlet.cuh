@@ -234,7 +234,7 @@ static __device__ __noinline__ int dir_rows_topk(int lane, const double* ring, i
                                           int E, int k, int* counts) {
   const int kc = k + 1;
   int tie = 0;
-  if (E <= 32) {
+  if (E <= 32 || r1 - r0 >= 32) {  // one lane per row (the caller batches rows)
     for (int64_t r = r0 + lane; r < r1; r += 32) {
       uint64_t key[KCAP];
       int ex[KCAP];
@@ -377,14 +377,13 @@ static __device__ __noinline__ int route_dirichlet_warp(int lane, int64_t T, int
                     2 * __popc(__ballot_sync(FS_FULL, cnt & 2) & lt) +
                     4 * __popc(__ballot_sync(FS_FULL, cnt & 4) & lt);
     int64_t vi = v + pre;
+    int e = (int)(vi - (vi / E) * E);  // one division per lane per window, then a counter
 #pragma unroll
     for (int j = 0; j < 4; j++) {
       if (!((acc_bits >> j) & 1u)) continue;
-      if (vi < total) {
-        const int e = (int)(vi % E);
-        ring[vi & (kDirRing - 1)] = val[j] / pop[e];
-      }
+      if (vi < total) ring[vi & (kDirRing - 1)] = val[j] / pop[e];
       vi++;
+      if (++e == E) e = 0;
     }
     int win = cnt;
 #pragma unroll
@@ -392,10 +391,13 @@ static __device__ __noinline__ int route_dirichlet_warp(int lane, int64_t T, int
     v += win;
     pos = 4 * (B + 32) + (uint64_t)carry;
     __syncwarp();
-    // completed rows
+    // completed rows, tallied 32 at a time (one lane each) once that many are
+    // buffered in the ring, or at the end of the call
     const int64_t done_rows = (v < total ? v : total) / E;
-    tie |= dir_rows(lane, ring, next_row, done_rows, E, k, counts);
-    next_row = done_rows;
+    if (done_rows - next_row >= 32 || v >= total || E <= 32) {
+      tie |= dir_rows(lane, ring, next_row, done_rows, E, k, counts);
+      next_row = done_rows;
+    }
     __syncwarp();
   }
   __syncwarp();

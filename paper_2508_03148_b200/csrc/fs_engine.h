@@ -35,7 +35,9 @@ struct RepState {
 
 constexpr int kJobLayers = 32;  // layers routed per job
 // dirichlet_skew router scratch per warp (fs_dirichlet.cuh): popularity[E] + a key ring
-constexpr int kDirRing = 2048;  // keys of unfinished rows + one window (>= 1023 + 128)
+// keys of up to 32 completed-but-untallied rows + one unfinished row + one window
+// (rows are tallied 32 at a time, one per lane): 32 x 1024 + 1023 + 128 < 2^16
+constexpr int kDirRing = 65536;
 constexpr int kDirScratch = FS_MAX_EXPERTS + kDirRing;  // doubles
 
 // A routing job: the uniform router calls of up to kJobLayers layers of one
@@ -44,9 +46,11 @@ constexpr int kDirScratch = FS_MAX_EXPERTS + kDirRing;  // doubles
 struct RouteJob {
   unsigned long long ctr;  // epoch (24 bits) | n_chunks (20 bits) | next chunk (20 bits)
   int32_t done;            // chunks finished
-  int32_t tie;             // a boundary tie was seen
+  int32_t tie;             // status: 0, FS_ERR_ROUTING_TIE or another routing error
   int64_t T;               // tokens (rows per layer)
-  int32_t E, k, nl, nseg, passes_per_chunk, pad;
+  int32_t E, k, nl, nseg, passes_per_chunk;
+  int32_t kind;            // 0: uniform, chunks of rows; 1: dirichlet_skew, one chunk per layer
+  double alpha;            // dirichlet_skew concentration
   uint64_t keys[kJobLayers][2];
 };
 

@@ -559,15 +559,41 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
     }
     __syncwarp();
   }
-  if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, 1);
+  if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, FS_ERR_ROUTING_TIE);
 }
+
+#if FS_LEARNED
+// dirichlet_skew: chunk c is the whole router call of layer c (its exponentials are
+// one stream with data-dependent word consumption); the claimant draws it with its
+// own scratch and stores the layer's tally.
+__device__ void dirichlet_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+                                int lane, int* tally, int my_slot) {
+  const int64_t T = __ldcg(&job->T);
+  const int E = __ldcg(&job->E), k = __ldcg(&job->k);
+  const double alpha = __ldcg(&job->alpha);
+  const uint64_t k0 = __ldcg(&job->keys[c][0]), k1 = __ldcg(&job->keys[c][1]);
+  const int st = route_dirichlet_warp(lane, T, E, k, alpha, k0, k1,
+                                      P.dir_scratch + (int64_t)my_slot * kDirScratch, tally);
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) counts[(int64_t)c * E + e] = tally[e];
+  if (st != FS_OK && lane == 0) atomicExch(&job->tie, st);
+}
+#endif
 
 // publish: completion is a release by lane 0 after __syncwarp (orders every
 // lane's tally atomics before it); private jobs (run by their owner alone)
 // skip it
 __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
-                              int lane, int* tally, bool publish) {
+                              int lane, int* tally, bool publish, int my_slot) {
   const int k = __ldcg(&job->k);
+#if FS_LEARNED
+  if (__ldcg(&job->kind) == 1) {
+    dirichlet_chunk(P, job, counts, c, lane, tally, my_slot);
+    __syncwarp();
+    if (publish && lane == 0) red_add_release_i32(&job->done, 1);
+    return;
+  }
+#endif
   if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane, tally);
 #if FS_KCAP_MAX > 4
   else if (k + 1 <= 9) process_chunk_k<9>(P, job, counts, c, lane, tally);
@@ -592,13 +618,13 @@ __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* cou
 #define FS_JOB_FN __device__ __forceinline__
 #endif
 FS_JOB_FN void drain_job(const EngineParams& P, RouteJob* job, int32_t* counts, int lane,
-                         int* tally) {
+                         int* tally, int my_slot) {
   for (int c; (c = claim_chunk(P, job, lane)) >= 0;)
-    process_chunk(P, job, counts, c, lane, tally, true);
+    process_chunk(P, job, counts, c, lane, tally, true, my_slot);
 }
 FS_JOB_FN void run_chunks(const EngineParams& P, RouteJob* job, int32_t* counts, int n, int lane,
-                          int* tally) {
-  for (int c = 0; c < n; c++) process_chunk(P, job, counts, c, lane, tally, false);
+                          int* tally, int my_slot) {
+  for (int c = 0; c < n; c++) process_chunk(P, job, counts, c, lane, tally, false, my_slot);
 }
 
 __device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slot) {
@@ -606,9 +632,10 @@ __device__ __forceinline__ int32_t* job_counts_of(const EngineParams& P, int slo
 }
 
 // Route layers [l0, l0+nl) of one batch; the tally of layer l0+j ends up at
-// job_counts_of(slot)[j*E ...]. Returns FS_OK or FS_ERR_ROUTING_TIE.
+// job_counts_of(slot)[j*E ...]. Returns FS_OK or a routing status (e.g.
+// FS_ERR_ROUTING_TIE). kind 1: dirichlet_skew, one chunk per layer.
 __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb, int64_t step,
-                             int l0, int nl, int64_t T, int* tally) {
+                             int l0, int nl, int64_t T, int* tally, int kind = 0) {
   const fs_instance_desc* d = I.d;
   RouteJob* job = &P.jobs[I.slot];
   int32_t* counts = job_counts_of(P, I.slot);
@@ -647,13 +674,16 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
     ppc = (int)((passes + kMaxChunks - 1) / kMaxChunks);
     n_chunks = (passes + ppc - 1) / ppc;
   }
+  if (kind == 1) n_chunks = nl;  // dirichlet_skew: a layer's stream is one chunk
   if (I.lane == 0) {
     job->T = T; job->E = E; job->k = k; job->nl = nl; job->nseg = nseg;
     job->passes_per_chunk = ppc; job->done = 0; job->tie = 0;
+    job->kind = kind; job->alpha = d->routing_alpha;
   }
   __syncwarp();
   __threadfence();
-  const bool shared = n_chunks >= 4;  // small jobs are not worth publishing
+  // small jobs are not worth publishing; a dirichlet layer always is
+  const bool shared = kind == 1 ? n_chunks >= 2 : n_chunks >= 4;
   if (I.lane == 0) {
     const unsigned long long epoch =
         ((ld_volatile_u64(&job->ctr) >> (2 * kChunkBits)) + 1) & 0xFFFFFFull;
@@ -665,14 +695,14 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
   }
   __syncwarp();
   if (shared) {
-    drain_job(P, job, counts, I.lane, tally);
+    drain_job(P, job, counts, I.lane, tally, I.slot);
     while (ld_acquire_i32(&job->done) < n_chunks) __nanosleep(64);
   } else {
-    run_chunks(P, job, counts, (int)n_chunks, I.lane, tally);
+    run_chunks(P, job, counts, (int)n_chunks, I.lane, tally, I.slot);
   }
   __threadfence();
   __syncwarp();
-  return ld_volatile_i32(&job->tie) ? FS_ERR_ROUTING_TIE : FS_OK;
+  return ld_volatile_i32(&job->tie);
 }
 
 // uniform routing with real draws goes through the job board; the trace policy
@@ -721,7 +751,7 @@ __device__ void help_route_jobs(const EngineParams& P, int lane, int my_slot, in
         m &= m - 1;
         const int sp = __shfl_sync(FS_FULL, s, pick);
         RouteJob* job = &P.jobs[sp];
-        drain_job(P, job, job_counts_of(P, sp), lane, tally);
+        drain_job(P, job, job_counts_of(P, sp), lane, tally, my_slot);
       }
     }
   }
@@ -1019,12 +1049,23 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
     return __dmul_rn((double)L, tot) + bt.pp;
   } else {
     const bool board = use_job_board(I.d, d->routing_policy, n);
+#if FS_LEARNED
+    // dirichlet_skew: the layers' router calls are independent streams, one chunk
+    // each, so idle warps take whole layers (the analytic costs then read the tally)
+    const bool dboard = d->routing_policy == FS_ROUTE_DIRICHLET && d->gg_forest == -1 && n > 0 &&
+                        d->top_k < d->num_experts && d->top_k >= 1 &&
+                        d->top_k <= FS_MAX_TOPK && d->num_experts <= FS_MAX_EXPERTS &&
+                        d->routing_alpha > 0;
+#else
+    const bool dboard = false;
+#endif
     const bool log_routes = P.log_enabled && P.log.routes;
     for (int l0 = 0; l0 < L; l0 += kLayerChunk) {
       const int lend = min(L, l0 + kLayerChunk);
       double lane_ffn = 0.0, lane_ratio = 1.0;
-      if (board) {
-        int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n, sm->counts);
+      if (board || dboard) {
+        int st = run_route_job(P, I, rd.prefix, 0, step, l0, lend - l0, n, sm->counts,
+                               dboard ? 1 : 0);
         if (st == FS_OK)
           st = moe_layers_lanes(I.lane, job_counts_of(P, I.slot), lend - l0, n, d->num_experts,
                                 d->top_k, d->d_model, d->expert_d_ff, d->ffn_matrices,
@@ -1037,11 +1078,11 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
       }
       for (int l = l0; l < lend; l++) {
         double ffn, ratio = 1.0;
-        if (board) {
+        if (board || dboard) {
           ffn = __shfl_sync(FS_FULL, lane_ffn, l - l0);
           ratio = __shfl_sync(FS_FULL, lane_ratio, l - l0);
           I.routing_calls++;
-          I.routing_draws += draws_of(d, FS_ROUTE_UNIFORM, n);
+          I.routing_draws += draws_of(d, d->routing_policy, n);
           if (log_routes) {
             load_job_layer(P, I, l - l0, sm);
             log_route(P, I, r, 0, step, l, n, sm);

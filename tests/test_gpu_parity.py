@@ -212,3 +212,28 @@ def test_dispatch_knobs_do_not_change_results(engine, env, monkeypatch):
     got = other.run(low)
     assert got.rows.tobytes() == want.rows.tobytes()
     assert np.array_equal(got.first_ns, want.first_ns) and np.array_equal(got.done_ns, want.done_ns)
+
+
+def test_per_variant_waves_match_solo_runs(engine):
+    """A heterogeneous batch runs as one wave per kernel variant (learned /
+    dirichlet, long-row, sweep, dense; fs_stage): every instance's outputs equal
+    its own single-instance run and the oracle's."""
+    from oracle import oracle
+    dsv3_dir = W.c4_colocated_ep(12, seed=5)
+    dsv3_dir["routing"] = {"policy": "dirichlet_skew", "alpha": 0.3}
+    mix_dir = W.c5_sweep_configs(4)[48 + 2]
+    mix_dir = copy.deepcopy(mix_dir)
+    mix_dir["routing"] = {"policy": "dirichlet_skew", "alpha": 1.0}
+    docs = (W.c5_sweep(n_seeds=1, n_requests=16)[::5]
+            + [W.c4_colocated_ep(10, seed=3), dsv3_dir, mix_dir, W.c3_pd(12, seed=4)])
+    specs = [instance_spec(parse_config(copy.deepcopy(d))) for d in docs]
+    batch = engine.run(lower(specs))
+    ref = oracle.run(lower(specs))
+    assert_same_raw(batch, ref)
+    for i in (0, len(docs) - 4, len(docs) - 3, len(docs) - 2, len(docs) - 1):
+        solo = engine.run(lower([specs[i]]))
+        o = int(lower(specs).descs[i]["req_offset"])
+        n = len(specs[i].requests)
+        assert solo.rows.tobytes() == batch.rows[i:i + 1].tobytes(), i
+        assert np.array_equal(solo.first_ns, batch.first_ns[o:o + n]), i
+        assert np.array_equal(solo.done_ns, batch.done_ns[o:o + n]), i
