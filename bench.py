@@ -55,7 +55,11 @@ def parse_args():
     ap.add_argument("--no-api", action="store_true", help="skip the simulate() end-to-end leg")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config (C1/C3/C4) batches")
-    ap.add_argument("--cpu-sample-seeds", type=int, default=8)
+    ap.add_argument("--cpu-sample-seeds", type=int, default=8,
+                    help="seeds per config of the main arm's cpu_baseline sample")
+    ap.add_argument("--reference-seeds", type=int, default=None,
+                    help="seeds per config the reference arm times (default: --seeds, the "
+                         "same workload as the GPU arm)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     return ap.parse_args()
 
@@ -74,9 +78,28 @@ def workload_docs(rank: int, n_seeds: int, n_requests: int):
 
 def lower_docs(docs):
     from paper_2508_03148_b200.api import instance_spec
-    from paper_2508_03148_b200.config import parse_config
+    from paper_2508_03148_b200.config import parse_many
     from paper_2508_03148_b200.lower import lower
-    return lower([instance_spec(parse_config(d)) for d in docs])
+    return lower([instance_spec(c) for c in parse_many(docs)])
+
+
+def routing_peak():
+    """The routing core's measured peak on this GPU model (scripts/micro/philox_peak.cu:
+    Philox4x64-10 blocks -> 32-bit keys -> top-3 of 8 -> tally, committed under
+    profiles/): keys/s of the rolled-loop code sim_kernel runs, at 8 warps per SM
+    (its occupancy) and the best over occupancies, and of the unrolled variant."""
+    path = os.path.join(ROOT, "profiles", "philox_peak_r2.json")
+    try:
+        rows = [json.loads(l) for l in open(path) if l.startswith('{"kernel"')]
+    except Exception:
+        return None
+    rolled8 = [r["G_keys_per_s"] for r in rows if r["kernel"] == "rolled" and r["warps_per_sm"] == 8]
+    rolled = [r["G_keys_per_s"] for r in rows if r["kernel"] == "rolled"]
+    unrolled = [r["G_keys_per_s"] for r in rows if r["kernel"].startswith("unrolled")]
+    if not rolled8:
+        return None
+    return {"rolled_8_warps_per_sm": rolled8[0] * 1e9, "rolled_best": max(rolled) * 1e9,
+            "unrolled_best": max(unrolled) * 1e9, "source": "profiles/philox_peak_r2.json"}
 
 
 def cpu_count() -> int:
@@ -297,6 +320,11 @@ def bench_attention_cost(eng, device: int, steps: int, warmup: int, n_batches: i
     return res
 
 
+def _dirichlet(doc: dict, alpha: float = 0.3) -> dict:
+    doc["routing"] = {"policy": "dirichlet_skew", "alpha": alpha}
+    return doc
+
+
 def bench_configs(device: int, reps: int = 2):
     """The other BASELINE.json configs as batches of independent seeds on one GPU:
     C1 (Llama-2-7B co-located, 1,000 requests), C3 (PD 70B, tight 30 GB decode
@@ -313,6 +341,8 @@ def bench_configs(device: int, reps: int = 2):
         "C3_pd_70b_tight_300req": (lambda s: W.c3_pd(300, seed=s, tight=True), 296),
         "C4_af_dsv3_m2_64req": (lambda s: W.c4_af(64, seed=s), 148),
         "C4_colocated_dsv3_ep8_64req": (lambda s: W.c4_colocated_ep(64, seed=s), 148),
+        "C4_colocated_dsv3_ep8_dirichlet0.3_64req": (lambda s: _dirichlet(W.c4_colocated_ep(64, seed=s)),
+                                                     148),
     }
     out = {}
     stream = torch.cuda.Stream(device=device)
@@ -342,6 +372,57 @@ def bench_configs(device: int, reps: int = 2):
                      "routing_draws": int(rows["routing_draws"].sum()),
                      "cpu_port_1core_iterations_per_s": int(ref.rows["iterations"][0]) / cpu_s}
     return out
+
+
+def routing_line(draws: int, step_ms: float) -> dict:
+    rate = draws / (step_ms / 1e3)
+    pk = routing_peak()
+    out = {"draws_per_step": draws, "draws_per_s": rate,
+           "note": "uniform-router Philox4x64-10 keys (T x E per call) drawn inside sim_kernel; "
+                   "frac = keys/s over the whole step against the routing core's measured peak "
+                   "at sim_kernel's occupancy (8 warps/SM)"}
+    if pk:
+        out.update({"peak": pk["rolled_8_warps_per_sm"], "frac": rate / pk["rolled_8_warps_per_sm"],
+                    "peak_best_occupancy": pk["rolled_best"], "peak_unrolled": pk["unrolled_best"],
+                    "peak_source": pk["source"]})
+    return out
+
+
+def bench_learned_sweep(device: int, seeds: int = 8, reps: int = 2):
+    """C5's 64 configs in learned mode (cost_model.mode learned with the C2 attention
+    forest, model.py:294-327): every iteration's attention cost is a 100-tree forest
+    prediction over the batch's attention_v1 features, inside sim_kernel's learned
+    variant. Device ms per batch (inputs resident) and iterations/s."""
+    import copy as _copy
+
+    import torch
+
+    from paper_2508_03148_b200.engine import Engine
+    model = os.path.join(ROOT, "tests", "golden", "forest_c2.json.gz")
+    if not os.path.exists(model):
+        return None
+    docs = workload_docs(0, seeds, 64)
+    for d in docs:
+        d["cost_model"] = {"mode": "learned", "attention_model": model}
+    low = lower_docs([_copy.deepcopy(d) for d in docs])
+    eng = Engine(device)
+    stream = torch.cuda.Stream(device=device)
+    eng.stage(low)
+    eng.launch(stream.cuda_stream)
+    torch.cuda.synchronize()
+    rows = eng.fetch(low, per_request=False).rows
+    ms = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.launch(stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    its = int(rows["iterations"].sum())
+    return {"workload": f"C5 64 configs x {seeds} seeds, learned attention (forest_c2, 100 trees)",
+            "instances": low.n_instances, "iterations": its, "ms": min(ms),
+            "iterations_per_s": its / (min(ms) / 1e3), "all_ok": bool((rows["status"] == 0).all())}
 
 
 def main():
@@ -533,8 +614,10 @@ def main():
         c2 = bench_attention_cost(eng, local, args.steps, args.warmup)
 
     configs = None
+    learned = None
     if rank == 0 and world == 1 and not args.no_configs:
         configs = bench_configs(local)
+        learned = bench_learned_sweep(local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -569,10 +652,7 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
             "issue": issue,
             "api_end_to_end": api,
-            "routing": {"draws_per_step": draws_per_step * world,
-                        "draws_per_s": draws_per_step * world / (max_ms / args.steps / 1e3),
-                        "note": "uniform-router Philox4x64-10 keys (T x E per call) drawn "
-                                "inside sim_kernel"},
+            "routing": routing_line(draws_per_step * world, max_ms / args.steps),
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps,
@@ -580,6 +660,7 @@ def main():
             "step_ms": step_ms,
             "c2_attention_cost": c2,
             "baseline_configs": configs,
+            "c5_learned": learned,
         }
         print(json.dumps(line))
     if world > 1:
@@ -592,7 +673,8 @@ def main_reference(args, rank, world):
         return
     threads = cpu_count()
     from oracle import oracle
-    docs = workload_docs(0, args.cpu_sample_seeds, args.requests)
+    ref_seeds = args.reference_seeds or args.seeds
+    docs = workload_docs(0, ref_seeds, args.requests)
     low = lower_docs(docs)
     oracle.load()
     times = []
@@ -605,15 +687,17 @@ def main_reference(args, rank, world):
             times.append(dt)
             its = int(res.rows["iterations"].sum())
     value = its * len(times) / sum(times)
-    sample = (f"C5 configs x {args.cpu_sample_seeds} seeds = {low.n_instances} instances "
+    sample = (f"C5 configs x {ref_seeds} seeds = {low.n_instances} instances "
               f"({its} iterations) per step on {threads} threads ({cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / len(times) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64+int64", "data": "synthetic",
             "config": {"workload": f"C5 design-space sweep: 64 configs x {args.seeds} seeds x "
-                                   f"{args.requests} requests per GPU (timed on a "
-                                   f"{args.cpu_sample_seeds}-seed sample)"},
+                                   f"{args.requests} requests per GPU"
+                                   + ("" if ref_seeds == args.seeds else
+                                      f" (timed on a {ref_seeds}-seed sample of every config)"),
+                       "instances_per_step": low.n_instances},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -45,7 +45,8 @@ extern "C" {
  * reported as FS_ERR_CAPACITY rather than silently truncated). */
 #define FS_MAX_PREFIX_BYTES 192   /* "{seed}:{cluster_id}/{idx}:" router-seed prefix   */
 #define FS_MAX_EXPERTS 1024       /* experts per MoE layer                              */
-#define FS_MAX_TOPK 16            /* top_k for uniform routing                         */
+#define FS_MAX_TOPK 16            /* top_k of the register top-(k+1) lists; larger     
+                                     top_k sorts whole rows (no limit below E)          */
 #define FS_MAX_MICRO_BATCHES 64   /* AF micro-batches per step                         */
 #define FS_MAX_REPLICAS 65536     /* replicas per instance (state spills to HBM)       */
 
@@ -80,8 +81,12 @@ enum fs_status {
   FS_ERR_TOPOLOGY_MISMATCH = 6,    /* costmodel/moe.py:19 TopologyMismatch                */
   FS_ERR_EMPTY_BATCH = 7,          /* costmodel/features.py:17 EmptyBatch                 */
   FS_ERR_INVALID_TOPK = 8,         /* costmodel/routing.py:21 InvalidTopK                 */
-  FS_ERR_ROUTING_TIE = 9,          /* exact key tie at the top-k boundary: argpartition's
-                                      choice is implementation-defined; flagged, not guessed */
+  FS_ERR_ROUTING_TIE = 9,          /* exact key tie at the top-k boundary: which tied
+                                      expert np.argpartition keeps depends on numpy's SIMD
+                                      dispatch on the host CPU (AVX2+ and baseline kernels
+                                      differ, tests/test_known_answers.py), so the engine
+                                      flags it rather than guess one host's answer
+                                      (probability ~E^2 2^-54 per row)               */
   FS_ERR_UNSUPPORTED = 10,         /* reserved: no current device path returns it          */
   FS_ERR_CAPACITY = 11,            /* engine limit (FS_MAX_*) exceeded                     */
   FS_ERR_INTERNAL = 12,            /* invariant violated inside the engine                 */

@@ -213,8 +213,11 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   std::vector<int> cls(n_instances);
   for (int i = 0; i < n_instances; i++) {
     const fs_instance_desc& d = descs[i];
+    // the extended (learned) kernel also carries dirichlet_skew routing and the
+    // full-row sort for top_k > FS_MAX_TOPK
     const bool lrn = d.attn_forest != -1 || d.gg_forest != -1 ||
-                     (d.has_moe && d.routing_policy == FS_ROUTE_DIRICHLET);
+                     (d.has_moe && d.routing_policy == FS_ROUTE_DIRICHLET) ||
+                     (d.has_moe && d.top_k > FS_MAX_TOPK && d.top_k < d.num_experts);
     int c;
     if (lrn) c = fs::kSimLearned;
     else if (d.has_moe && d.num_experts >= 64 && !no_longrow) c = fs::kSimLongRow;
@@ -365,7 +368,8 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   bool dirichlet = false;
   for (int i = 0; i < n_instances; i++)
     dirichlet |= descs[i].has_moe && (descs[i].routing_policy == FS_ROUTE_DIRICHLET ||
-                                      descs[i].gg_forest != -1);  // learned MoE: entropy scratch
+                                      descs[i].gg_forest != -1 ||  // learned MoE: entropy
+                                      descs[i].top_k > FS_MAX_TOPK);  // row sort buffer
   if (dirichlet) {
     FS_CHECK(e->dir_scratch.ensure((size_t)P.n_slots * fs::kDirScratch * sizeof(double)));
     P.dir_scratch = e->dir_scratch.as<double>();
@@ -400,16 +404,24 @@ int fs_launch_async(fs_engine* e, void* stream) {
   // One wave per kernel variant, back to back on the stream: different variants on
   // the same SMs fight over instruction fetch (the C5 sweep took 280 ms with its MoE
   // and dense instances mixed, 184 + 71 ms as separate waves).
+  // an event trace is recorded by the extended variant only (fs_sim.cuh tracing())
+  const bool traced = e->params.log_enabled && e->params.log.events != nullptr;
   for (int w = 0; w < e->n_waves; w++) {
     fs::EngineParams p = e->params;
     p.n_inst = e->waves[w].count;
     p.order = e->params.order + e->waves[w].start;
     p.n_slots = e->waves[w].slots;
+    int variant = e->waves[w].variant;
+    if (traced && variant != fs::kSimLearned) {
+      variant = fs::kSimLearned;
+      p.n_slots = std::min(p.n_slots, fs::simulation_slots(e->n_sms, p.n_inst, variant,
+                                                           e->sim_ctas, p.jobs != nullptr));
+    }
     if (w > 0) {
       FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
       FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
     }
-    e->last_launches += fs::launch_simulation(p, e->waves[w].variant, s);
+    e->last_launches += fs::launch_simulation(p, variant, s);
   }
   e->last_launches += fs::launch_metrics(e->params, s);
   FS_CHECK(cudaGetLastError());
@@ -644,7 +656,7 @@ int fs_route_tokens(fs_engine* e, const int64_t* tokens, const uint64_t* seeds, 
   FS_CHECK(e->c_counts.ensure(nc * 4));
   FS_CHECK(e->c_status.ensure((size_t)std::max(n_calls, 1) * 4));
   double* scratch = nullptr;
-  if (policy == FS_ROUTE_DIRICHLET) {
+  if (policy == FS_ROUTE_DIRICHLET || (top_k > FS_MAX_TOPK && top_k < num_experts)) {
     FS_CHECK(e->c_scratch.ensure((size_t)fs::route_scratch_warps(n_calls) * fs::kDirScratch * 8));
     scratch = e->c_scratch.as<double>();
   }

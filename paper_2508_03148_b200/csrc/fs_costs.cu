@@ -750,7 +750,7 @@ __global__ void route_kernel(const int64_t* tokens, const uint64_t* seeds, int n
     int st;
     const int64_t T = tokens[c];
     if (!(1 <= k && k <= E)) st = FS_ERR_INVALID_TOPK;
-    else if (E > FS_MAX_EXPERTS || (k < E && k > FS_MAX_TOPK)) st = FS_ERR_CAPACITY;
+    else if (E > FS_MAX_EXPERTS) st = FS_ERR_CAPACITY;
     else if (T < 0) st = FS_ERR_ROUTING;
     else if (policy != FS_ROUTE_UNIFORM && policy != FS_ROUTE_DIRICHLET) st = FS_ERR_ROUTING;
     else {
@@ -758,6 +758,9 @@ __global__ void route_kernel(const int64_t* tokens, const uint64_t* seeds, int n
       routing_key(seeds[c], key);
       if (policy == FS_ROUTE_DIRICHLET && T > 0 && k < E)
         st = route_dirichlet_warp(lane, T, E, k, alpha, key[0], key[1],
+                                  scratch + (int64_t)gw * kDirScratch, sm_counts[w]);
+      else if (T > 0 && k < E && k > FS_MAX_TOPK)
+        st = route_uniform_sorted(lane, T, E, k, key[0], key[1],
                                   scratch + (int64_t)gw * kDirScratch, sm_counts[w]);
       else
         st = route_uniform_warp(lane, T, E, k, key[0], key[1], sm_counts[w]);

@@ -284,9 +284,31 @@ static __device__ __noinline__ int dir_rows_topk(int lane, const double* ring, i
   return tie;
 }
 
+// top_k > FS_MAX_TOPK: each completed row sorted whole (fs_route.cuh select_sorted)
+static __device__ __noinline__ int dir_rows_sorted(int lane, const double* ring, int64_t r0,
+                                                   int64_t r1, int E, int k, int* counts,
+                                                   double* sortbuf) {
+  uint64_t* key = reinterpret_cast<uint64_t*>(sortbuf);
+  uint64_t* idx = key + FS_MAX_EXPERTS;
+  int tie = 0;
+  for (int64_t r = r0; r < r1; r++) {
+    const int64_t base = r * (int64_t)E;
+    for (int e = lane; e < E; e += 32) {
+      key[e] = (uint64_t)__double_as_longlong(ring[(base + e) & (kDirRing - 1)]);
+      idx[e] = e;
+    }
+    __syncwarp();
+    tie |= select_sorted(lane, key, idx, E, k, counts);
+  }
+  return tie;
+}
+
 __device__ __forceinline__ int dir_rows(int lane, const double* ring, int64_t r0, int64_t r1,
                                         int E, int k, int* counts) {
   if (r0 >= r1) return 0;
+  if (k > FS_MAX_TOPK)  // the ring sits at scratch + FS_MAX_EXPERTS (route_dirichlet_warp)
+    return dir_rows_sorted(lane, ring, r0, r1, E, k, counts,
+                           const_cast<double*>(ring) - FS_MAX_EXPERTS + kSortOffset);
   if (k + 1 <= 4) return dir_rows_topk<4>(lane, ring, r0, r1, E, k, counts);
   if (k + 1 <= 9) return dir_rows_topk<9>(lane, ring, r0, r1, E, k, counts);
   return dir_rows_topk<FS_MAX_TOPK + 1>(lane, ring, r0, r1, E, k, counts);
@@ -299,7 +321,7 @@ static __device__ __noinline__ int route_dirichlet_warp(int lane, int64_t T, int
                                                  uint64_t k0, uint64_t k1, double* scratch,
                                                  int* counts) {
   if (!(alpha > 0)) return FS_ERR_ROUTING;
-  if (k > FS_MAX_TOPK || E > FS_MAX_EXPERTS) return FS_ERR_CAPACITY;
+  if (E > FS_MAX_EXPERTS) return FS_ERR_CAPACITY;
   for (int e = lane; e < E; e += 32) counts[e] = 0;
   double* pop = scratch;
   double* ring = scratch + FS_MAX_EXPERTS;

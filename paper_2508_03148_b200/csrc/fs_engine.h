@@ -38,7 +38,10 @@ constexpr int kJobLayers = 32;  // layers routed per job
 // keys of up to 32 completed-but-untallied rows + one unfinished row + one window
 // (rows are tallied 32 at a time, one per lane): 32 x 1024 + 1023 + 128 < 2^16
 constexpr int kDirRing = 65536;
-constexpr int kDirScratch = FS_MAX_EXPERTS + kDirRing;  // doubles
+// per-warp scratch (doubles): popularity[E] | ring | sort buffer for top_k > FS_MAX_TOPK
+// (FS_MAX_EXPERTS keys + FS_MAX_EXPERTS indices, fs_route.cuh select_sorted)
+constexpr int kSortOffset = FS_MAX_EXPERTS + kDirRing;
+constexpr int kDirScratch = kSortOffset + 2 * FS_MAX_EXPERTS;
 
 // A routing job: the uniform router calls of up to kJobLayers layers of one
 // batch (routing.py:65-113, one call per layer), split into chunks of rows

@@ -117,6 +117,67 @@ __device__ int route_uniform_warp_k(int lane, int64_t T, int E, int k, uint64_t 
   return tie ? FS_ERR_ROUTING_TIE : FS_OK;
 }
 
+// ---- top_k > FS_MAX_TOPK: a full sort of the row ------------------------------------
+// Rows too wide for the register top-(k+1) lists are sorted whole: n (key, expert)
+// pairs in this warp's global scratch (L1/L2 resident), a warp bitonic network over
+// the next power of two, then the k smallest are tallied. Keys are order-preserving
+// u64s (the 53-bit draw; or a positive double's IEEE bits). Equal keys at positions
+// k-1 and k are an exact boundary tie. Returns 1 on a tie.
+__device__ inline int select_sorted(int lane, uint64_t* key, uint64_t* idx, int n, int k,
+                                    int* counts) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + lane; i < m; i += 32) { key[i] = ~0ull; idx[i] = 0; }
+  __syncwarp();
+  for (int size = 2; size <= m; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < m / 2; t += 32) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint64_t a = key[lo], b = key[hi];
+        if ((a > b) == up) {
+          key[lo] = b; key[hi] = a;
+          const uint64_t x = idx[lo];
+          idx[lo] = idx[hi]; idx[hi] = x;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int j = lane; j < k; j += 32) atomicAdd(&counts[(int)idx[j]], 1);
+  __syncwarp();
+  return key[k - 1] == key[k] ? 1 : 0;
+}
+
+// route_tokens uniform for top_k > FS_MAX_TOPK: row by row, the row's E draws in
+// Philox blocks spread over the lanes, then select_sorted.
+__device__ inline int route_uniform_sorted(int lane, int64_t T, int E, int k, uint64_t k0,
+                                           uint64_t k1, double* scratch, int* counts) {
+  uint64_t* key = reinterpret_cast<uint64_t*>(scratch + kSortOffset);
+  uint64_t* idx = key + FS_MAX_EXPERTS;
+  for (int e = lane; e < E; e += 32) counts[e] = 0;
+  __syncwarp();
+  int tie = 0;
+  for (int64_t r = 0; r < T; r++) {
+    const uint64_t n0 = (uint64_t)r * E, n1 = n0 + E;
+    for (uint64_t b = (n0 >> 2) + lane; b <= (n1 - 1) >> 2; b += 32) {
+      const U4 blk = philox4x64_10(b + 1, k0, k1);
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint64_t n = 4 * b + j;
+        if (n >= n0 && n < n1) {
+          key[n - n0] = blk.v[j] >> 11;
+          idx[n - n0] = n - n0;
+        }
+      }
+    }
+    __syncwarp();
+    tie |= select_sorted(lane, key, idx, E, k, counts);
+  }
+  return tie ? FS_ERR_ROUTING_TIE : FS_OK;
+}
+
 __device__ inline int route_uniform_warp(int lane, int64_t T, int E, int k, uint64_t k0,
                                          uint64_t k1, int* counts) {
   if (k + 1 <= 4) return route_uniform_warp_k<4>(lane, T, E, k, k0, k1, counts);

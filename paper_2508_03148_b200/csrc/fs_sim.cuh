@@ -283,7 +283,16 @@ __device__ int route_layer(const EngineParams& P, const Inst& I, int policy, int
     return FS_OK;
   }
   if (T == 0 || k == E || policy == FS_ROUTE_UNIFORM) {
-    if (T > 0 && k < E && k > FS_MAX_TOPK) return FS_ERR_CAPACITY;
+    if (T > 0 && k < E && k > FS_MAX_TOPK) {
+#if FS_LEARNED  // rows sorted whole; instances with such a top_k run in this variant
+      if (!P.dir_scratch) return FS_ERR_INTERNAL;
+      __syncwarp();
+      return route_uniform_sorted(I.lane, T, E, k, k0, k1,
+                                  P.dir_scratch + (int64_t)I.slot * kDirScratch, sm->counts);
+#else
+      return FS_ERR_INTERNAL;  // host dispatch error: top_k > FS_MAX_TOPK runs in `learned`
+#endif
+    }
     __syncwarp();
     return route_uniform_warp(I.lane, T, E, k, k0, k1, sm->counts);
   }
@@ -609,8 +618,8 @@ __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* cou
 // instance state is saved once per job around the call, and the routing loop
 // inside gets the register file to itself (one copy of the code for owners and
 // helpers alike).
-#ifndef FS_JOB_NOINLINE  // 0 measured best (313 vs 340 ms for the C5 sweep)
-#define FS_JOB_NOINLINE 0
+#ifndef FS_JOB_NOINLINE  // round 1: 0 best (313 vs 340 ms); round 2, after the event-trace
+#define FS_JOB_NOINLINE 1  // call sites: 1 best (227-234 vs 238-239 ms for the C5 sweep)
 #endif
 #if FS_JOB_NOINLINE
 #define FS_JOB_FN __device__ __noinline__
@@ -1054,8 +1063,7 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
     // each, so idle warps take whole layers (the analytic costs then read the tally)
     const bool dboard = d->routing_policy == FS_ROUTE_DIRICHLET && d->gg_forest == -1 && n > 0 &&
                         d->top_k < d->num_experts && d->top_k >= 1 &&
-                        d->top_k <= FS_MAX_TOPK && d->num_experts <= FS_MAX_EXPERTS &&
-                        d->routing_alpha > 0;
+                        d->num_experts <= FS_MAX_EXPERTS && d->routing_alpha > 0;
 #else
     const bool dboard = false;
 #endif
@@ -1120,8 +1128,15 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
 }
 
 // ---- optional event trace (fs_event_rec at index seq; one lane writes) ------------------
+// Event traces (run_one / make_simulation().run()) are recorded by the extended
+// variant only (fs_launch_async runs a traced batch there): in the sweep kernels the
+// trace call sites compile away instead of costing instruction fetch.
 __device__ __forceinline__ bool tracing(const EngineParams& P) {
+#if FS_LEARNED
   return P.log_enabled && P.log.events != nullptr;
+#else
+  return false;
+#endif
 }
 __device__ void trace_put(const EngineParams& P, const Inst& I, int64_t seq, int64_t t, int kind,
                           int replica, int32_t a, int32_t b, int32_t c, int64_t x) {

@@ -623,6 +623,32 @@ def capacity_scenarios() -> dict[str, dict]:
     return out
 
 
+def largek_fixtures() -> dict:
+    """top_k above the round-1 engine bound of 16: route_tokens counts (uniform and
+    dirichlet_skew) and two whole simulations of a 64-expert model with top_k 20 / 24."""
+    from frontier_sim.costmodel.routing import route_tokens
+    calls = []
+    for (T, E, k) in [(3, 32, 17), (40, 64, 20), (7, 64, 40), (5, 256, 100), (2, 256, 255),
+                      (9, 1024, 300)]:
+        for seed in (0, 5, 3735928559):
+            for policy, alpha in (("uniform", 0.3), ("dirichlet_skew", 0.3), ("dirichlet_skew", 2.0)):
+                a = route_tokens(T, E, k, policy=policy, seed=seed, alpha=alpha)
+                calls.append([T, E, k, seed, policy, alpha, list(a.counts)])
+    sims = {}
+    base = W.c5_sweep_configs(12)[48 + 1]
+    for name, k, routing in (("moe64_k20_uniform", 20, None),
+                             ("moe64_k24_dirichlet", 24, {"policy": "dirichlet_skew", "alpha": 0.5})):
+        d = copy.deepcopy(base)
+        d["model"]["moe"] = {"num_experts": 64, "top_k": k, "expert_d_ff": 2048}
+        d["model"]["num_layers"] = 6
+        d["seed"] = 21
+        if routing:
+            d["routing"] = routing
+        sims[name] = record(d, with_batches=True, with_routes=True)
+        print(name, sims[name].get("iterations"), sims[name].get("error"))
+    return {"route_calls": calls, "scenarios": sims}
+
+
 def write(name: str, payload) -> None:
     payload = {"numpy": np.__version__, "python": sys.version.split()[0], "data": payload}
     path = os.path.join(HERE, f"{name}.json.gz")
@@ -649,6 +675,8 @@ def main() -> None:
             print(name, sc[name].get("iterations"), sc[name].get("error"),
                   f"{sc[name]['wall_s']:.2f}s")
         write("scenarios", sc)
+    if only is not None and "largek" in only:
+        write("largek", largek_fixtures())
     if only is not None and "capacity" in only:
         cap = {}
         for name, doc in capacity_scenarios().items():

@@ -67,3 +67,34 @@ def test_long_prefix_router_seeds_device(engine):
             want.append(int.from_bytes(hashlib.sha256(msg.encode()).digest()[:4], "big"))
     got = engine.router_seeds(prefixes, list(range(len(prefixes))), mbs, steps, layers)
     assert got.tolist() == want
+
+
+# ---- top_k > 16 (tests/golden/largek.json.gz, make_golden.py --only largek) ----------------
+
+@pytest.fixture(scope="module")
+def golden_largek():
+    return load_golden("largek")["data"]
+
+
+def test_oracle_large_topk(golden_largek):
+    from oracle import oracle
+    for T, E, k, seed, policy, alpha, counts in golden_largek["route_calls"]:
+        got, st = oracle.route(T, E, k, policy, seed, alpha)
+        assert st == 0 and list(got) == counts, (T, E, k, seed, policy)
+    sc = golden_largek["scenarios"]
+    res = run_backend("oracle", [g["config"] for g in sc.values()], routes=True)
+    bad = {n: compare_to_golden(r, g) for (n, g), r in zip(sc.items(), res)}
+    assert {n: b for n, b in bad.items() if b} == {}
+
+
+@pytest.mark.gpu
+def test_device_large_topk(engine, golden_largek):
+    import numpy as np
+    for T, E, k, seed, policy, alpha, counts in golden_largek["route_calls"]:
+        got, st = engine.route_tokens(np.array([T]), np.array([seed], dtype=np.uint64), E, k,
+                                      policy, alpha)
+        assert st[0] == 0 and got[0].tolist() == counts, (T, E, k, seed, policy)
+    sc = golden_largek["scenarios"]
+    res = run_backend(engine, [g["config"] for g in sc.values()], routes=True)
+    bad = {n: compare_to_golden(r, g) for (n, g), r in zip(sc.items(), res)}
+    assert {n: b for n, b in bad.items() if b} == {}

@@ -79,3 +79,40 @@ def test_python_sum_of_identical_layers_is_one_rounded_product():
     for x in xs:
         for L in (1, 2, 3, 7, 32, 61, 80, 127, 128, rng.randint(1, 5000)):
             assert sum([x] * L) == L * x, (x, L)
+
+
+_TIE_PROBE = r"""
+import hashlib, numpy as np
+rng = np.random.default_rng(0)
+out = []
+for trial in range(600):
+    E = int(rng.choice([8, 16, 60, 256])); k = int(rng.integers(1, min(E, 17)))
+    keys = rng.random(E); order = np.argsort(keys, kind="stable")
+    keys[order[k]] = keys[order[k - 1]]          # k-th and (k+1)-th smallest tie exactly
+    out.append(tuple(sorted(np.argpartition(keys[None, :], k - 1, axis=1)[0, :k].tolist())))
+print(hashlib.sha256(repr(out).encode()).hexdigest())
+"""
+
+
+def test_argpartition_boundary_ties_depend_on_numpy_simd_dispatch():
+    """Why an exact tie at the top-k boundary is FS_ERR_ROUTING_TIE rather than an
+    answer: routing.py:110 picks the experts with np.argpartition, whose choice
+    between two equal keys is not a property of the reference but of numpy's
+    SIMD dispatch on the host CPU (the same rows give different experts with the
+    AVX2+ kernels and with the baseline ones). A tie has probability ~E^2 2^-54
+    per row; the engine reports it instead of guessing one host's answer."""
+    import os
+    import subprocess
+    import sys
+    base = dict(os.environ)
+    simd = subprocess.run([sys.executable, "-c", _TIE_PROBE], capture_output=True, text=True,
+                          env=base)
+    off = dict(base, NPY_DISABLE_CPU_FEATURES="AVX2 FMA3 AVX512F AVX512CD AVX512_SKX "
+                                             "AVX512_CLX AVX512_CNL AVX512_ICL AVX512_SPR")
+    scalar = subprocess.run([sys.executable, "-c", _TIE_PROBE], capture_output=True, text=True,
+                            env=off)
+    if simd.returncode or scalar.returncode:
+        pytest.skip("numpy SIMD dispatch cannot be switched here")
+    if simd.stdout == scalar.stdout:
+        pytest.skip("this host's numpy has no SIMD argpartition kernel")
+    assert simd.stdout != scalar.stdout
