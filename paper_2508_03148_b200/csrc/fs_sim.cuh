@@ -345,6 +345,9 @@ constexpr int kMaxChunks = 1 << 18;
 #define FS_CHUNK_BLOCKS 96
 #endif
 constexpr int kChunkBlocks = FS_CHUNK_BLOCKS;
+#ifndef FS_NSEG_ROWS  // rows are split into lane segments while rows * nseg stays below this
+#define FS_NSEG_ROWS 64  // 64: C5 224-226 ms; 256: 225-228; 2048 (round 1): ~228; 4096: 232-236
+#endif
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
   return *reinterpret_cast<const volatile unsigned long long*>(p);
@@ -672,7 +675,7 @@ __device__ int run_route_job(const EngineParams& P, Inst& I, int prefix, int mb,
   // carries >= ~16 Philox blocks per lane so claims and fences stay cheap
   const int64_t rows = (int64_t)nl * T;
   int nseg = 1;
-  while (nseg < 32 && (nseg * 2) * 4 <= E && rows * nseg < 2048) nseg *= 2;
+  while (nseg < 32 && (nseg * 2) * 4 <= E && rows * nseg < FS_NSEG_ROWS) nseg *= 2;
   const int rpp = 32 / nseg;
   const int64_t passes = (rows + rpp - 1) / rpp;
   const int blocks_per_pass = ((E + nseg - 1) / nseg + 3) / 4 + 1;
