@@ -130,12 +130,14 @@ __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, 
 }
 
 // ---- event heap (lane 0 mutates, the popped event is broadcast) ----------------
+// Only lane 0 ever reads or writes heap memory, so no warp barrier guards it; the
+// other lanes track the size (I.hn) and the sequence counter in their registers
+// and receive the popped event by shuffle.
 __device__ __forceinline__ bool hev_less(const HEv& a, const HEv& b) {
   return a.t < b.t || (a.t == b.t && a.seq < b.seq);
 }
 __device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   if (t < I.now) { fail(I, FS_ERR_SCHEDULING_IN_PAST, kind); return; }
-  __syncwarp();
   if (I.lane == 0) {
     HEv e;
     e.t = t; e.seq = I.seq; e.kind = kind; e.a = a; e.b = b;
@@ -151,12 +153,10 @@ __device__ void heap_push(Inst& I, int64_t t, int kind, int a, int64_t b) {
   }
   I.hn++;
   I.seq++;
-  __syncwarp();
 }
 __device__ HEv heap_pop(Inst& I) {
   HEv top;
   top.t = 0; top.seq = 0; top.kind = 0; top.a = 0; top.b = 0;
-  __syncwarp();
   if (I.lane == 0) {
     top = I.heap[0];
     const int n = I.hn - 1;
@@ -174,7 +174,6 @@ __device__ HEv heap_pop(Inst& I) {
     if (n > 0) I.heap[i] = last;
   }
   I.hn--;
-  __syncwarp();
   top.t = __shfl_sync(FS_FULL, top.t, 0);
   top.kind = __shfl_sync(FS_FULL, top.kind, 0);
   top.a = __shfl_sync(FS_FULL, top.a, 0);
