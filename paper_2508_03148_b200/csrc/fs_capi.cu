@@ -69,10 +69,11 @@ struct fs_engine {
   int n_moe = 0;         // MoE instances of the staged batch (first in the order)
   // waves: instances bucketed by kernel variant, consecutive in the order array
   struct Wave { int variant, start, count, slots; };
-  Wave waves[4];
+  Wave waves[5];
   int n_waves = 0;
   int split_families = 1;  // FS_SPLIT_FAMILIES: MoE and dense instances in separate waves
   int dense_variant = 1;   // FS_DENSE_VARIANT: dense instances on the MoE-free kernel
+  int comoe_variant = 1;   // FS_COMOE_VARIANT: co-located MoE instances on their own kernel
   // routing job geometry (environment knobs read at fs_create)
   int sim_ctas = 0;          // FS_SIM_CTAS_PER_SM (0 = as many as fit)
   int chunk_blocks = 96;     // FS_CHUNK_BLOCKS: Philox blocks per lane per job chunk
@@ -135,6 +136,7 @@ int fs_create(int device, fs_engine** out) {
   e->sim_ctas = env_int("FS_SIM_CTAS_PER_SM", 0);
   e->split_families = env_int("FS_SPLIT_FAMILIES", 1);
   e->dense_variant = env_int("FS_DENSE_VARIANT", 1);
+  e->comoe_variant = env_int("FS_COMOE_VARIANT", 1);
   e->chunk_blocks = env_int("FS_CHUNK_BLOCKS", 96);
   if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete e;
@@ -221,6 +223,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
     int c;
     if (lrn) c = fs::kSimLearned;
     else if (d.has_moe && d.num_experts >= 64 && !no_longrow) c = fs::kSimLongRow;
+    else if (d.has_moe && d.mode == FS_MODE_COLOCATED && e->comoe_variant) c = fs::kSimCoMoe;
     else if (d.has_moe || !e->dense_variant) c = fs::kSimAnalytic;
     else c = fs::kSimDense;
     cls[i] = c;
@@ -230,13 +233,14 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
     for (int i = 0; i < n_instances; i++) {
       if (cls[i] == fs::kSimLearned) v = fs::kSimLearned;
       else if (cls[i] == fs::kSimLongRow && v != fs::kSimLearned) v = fs::kSimLongRow;
-      else if (cls[i] == fs::kSimAnalytic && v == fs::kSimDense) v = fs::kSimAnalytic;
+      else if ((cls[i] == fs::kSimAnalytic || cls[i] == fs::kSimCoMoe) && v == fs::kSimDense)
+        v = fs::kSimAnalytic;
     }
     for (int i = 0; i < n_instances; i++) cls[i] = v;
   }
-  static const int kWaveOrder[4] = {fs::kSimLearned, fs::kSimLongRow, fs::kSimAnalytic,
-                                    fs::kSimDense};
-  auto rank_of = [&](int c) { for (int k = 0; k < 4; k++) if (kWaveOrder[k] == c) return k; return 4; };
+  static const int kWaveOrder[5] = {fs::kSimLearned, fs::kSimLongRow, fs::kSimAnalytic,
+                                    fs::kSimCoMoe, fs::kSimDense};
+  auto rank_of = [&](int c) { for (int k = 0; k < 5; k++) if (kWaveOrder[k] == c) return k; return 5; };
   std::vector<int32_t> order(n_instances);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {

@@ -30,6 +30,7 @@ int simulation_slots(int n_sms, int n_inst, int variant, int ctas_per_sm, bool h
   if (variant == kSimLearned) return learned::slots(n_sms, n_inst, ctas_per_sm, helpers);
   if (variant == kSimLongRow) return longrow::slots(n_sms, n_inst, ctas_per_sm, helpers);
   if (variant == kSimDense) return dense::slots(n_sms, n_inst, ctas_per_sm, helpers);
+  if (variant == kSimCoMoe) return comoe::slots(n_sms, n_inst, ctas_per_sm, helpers);
   return analytic::slots(n_sms, n_inst, ctas_per_sm, helpers);
 }
 
@@ -37,6 +38,7 @@ int launch_simulation(const EngineParams& p, int variant, void* stream) {
   if (variant == kSimLearned) return learned::launch(p, stream);
   if (variant == kSimLongRow) return longrow::launch(p, stream);
   if (variant == kSimDense) return dense::launch(p, stream);
+  if (variant == kSimCoMoe) return comoe::launch(p, stream);
   return analytic::launch(p, stream);
 }
 

@@ -119,13 +119,18 @@ namespace longrow {
 int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
 int launch(const EngineParams& p, void* stream);
 }  // namespace longrow
+namespace comoe {
+int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
+int launch(const EngineParams& p, void* stream);
+}  // namespace comoe
 namespace dense {
 int slots(int n_sms, int n_inst, int ctas_per_sm, bool helpers);
 int launch(const EngineParams& p, void* stream);
 }  // namespace dense
 // simulation kernel variants: analytic (the sweep kernel), learned (learned models,
 // dirichlet routing), longrow (analytic, MoE rows of >= 64 experts), dense (no MoE)
-enum SimVariant { kSimAnalytic = 0, kSimLearned = 1, kSimLongRow = 2, kSimDense = 3 };
+enum SimVariant { kSimAnalytic = 0, kSimLearned = 1, kSimLongRow = 2, kSimDense = 3,
+                  kSimCoMoe = 4 };
 // ctas_per_sm <= 0: as many simulation CTAs per SM as fit
 int simulation_slots(int n_sms, int n_inst, int variant, int ctas_per_sm, bool helpers);
 int launch_simulation(const EngineParams& p, int variant, void* stream);

@@ -49,6 +49,11 @@
 #ifndef FS_DIR_IN_ANALYTIC
 #define FS_DIR_IN_ANALYTIC 0
 #endif
+#ifndef FS_MODES  // serving modes compiled in: 1 colocated | 2 pd | 4 af
+#define FS_MODES 7
+#endif
+#define FS_HAS_PD ((FS_MODES & 2) != 0)
+#define FS_HAS_AF ((FS_MODES & 4) != 0)
 #ifndef FS_DENSE_ONLY  // the MoE paths compiled out (the dense wave's kernel variant)
 #define FS_DENSE_ONLY 0
 #endif
@@ -1608,7 +1613,7 @@ __device__ void co_batch_start(const EngineParams& P, Inst& I, int r, WarpSmem* 
       s.used += A.charge;
       start_prefill(P, I, r, s, rd, A, sm);
     } else if (s.rlen) {
-      if (I.mode == FS_MODE_AF) af_start_step(P, I, s, rd, sm);
+      if (FS_HAS_AF && I.mode == FS_MODE_AF) af_start_step(P, I, s, rd, sm);
       else start_decode(P, I, r, s, rd, sm);
     } else if (s.qlen) {
       fail(I, FS_ERR_REQUEST_CANNOT_FIT, queue_head(I, r, s));
@@ -2014,6 +2019,8 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
 
   if (I.R > FS_MAX_REPLICAS || (d->has_moe && d->num_experts > FS_MAX_EXPERTS)) fail(I, FS_ERR_CAPACITY, 0);
   if (FS_DENSE_ONLY && d->has_moe) fail(I, FS_ERR_INTERNAL, 9);  // host dispatch error
+  if ((I.mode == FS_MODE_PD && !FS_HAS_PD) || (I.mode == FS_MODE_AF && !FS_HAS_AF))
+    fail(I, FS_ERR_INTERNAL, 10);  // host dispatch error: mode not compiled into this variant
 #if FS_LEARNED
   {
     const int fsel[2] = {d->attn_forest, d->gg_forest};
@@ -2051,18 +2058,18 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
       const int req = I.cursor++;
       if (tracing(P) && lane == 0)
         trace_put(P, I, req, ta, FS_EV_REQUEST_ARRIVAL, -1, req, 0, 0, 0);
-      if (I.mode == FS_MODE_PD) pd_arrival(P, I, req);
+      if (FS_HAS_PD && I.mode == FS_MODE_PD) pd_arrival(P, I, req);
       else co_arrival(P, I, req);
     } else {
       const HEv e = heap_pop(I);
       I.now = e.t;
       if (e.kind == K_BATCH_START) {
-        if (I.mode == FS_MODE_PD) pd_batch_start(P, I, e.a, sm);
+        if (FS_HAS_PD && I.mode == FS_MODE_PD) pd_batch_start(P, I, e.a, sm);
         else co_batch_start(P, I, e.a, sm);
       } else if (e.kind == K_BATCH_COMPLETE) {
-        if (I.mode == FS_MODE_PD) pd_batch_complete(P, I, e.a, e.b);
+        if (FS_HAS_PD && I.mode == FS_MODE_PD) pd_batch_complete(P, I, e.a, e.b);
         else co_batch_complete(P, I, e.a, e.b);
-      } else if (e.kind == K_KV_DONE) {
+      } else if (FS_HAS_PD && e.kind == K_KV_DONE) {
         pd_transfer_done(P, I, e.a, (int)e.b);
       }
     }

@@ -16,6 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libfrontier_b200.so")
 OBJ = os.path.join(HERE, "lib", "obj")
 SOURCES = ["fs_engine.cu", "fs_engine_learned.cu", "fs_engine_longrow.cu", "fs_engine_dense.cu",
+           "fs_engine_comoe.cu",
            "fs_metrics.cu",
            "fs_costs.cu", "fs_capi.cu"]
 HEADERS = ["fs_device.cuh", "fs_route.cuh", "fs_engine.h", "fs_forest.cuh", "fs_sim.cuh",

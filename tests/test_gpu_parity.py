@@ -197,7 +197,7 @@ def test_baseline_full_sizes_vs_oracle_with_invariants(engine):
         assert r.iterations == len(r.batches)
 
 
-@pytest.mark.parametrize("env", [{"FS_SPLIT_FAMILIES": "0"}, {"FS_DENSE_VARIANT": "0"},
+@pytest.mark.parametrize("env", [{"FS_SPLIT_FAMILIES": "0"}, {"FS_DENSE_VARIANT": "0"}, {"FS_COMOE_VARIANT": "0"},
                                  {"FS_CHUNK_BLOCKS": "16"}, {"FS_NO_LONGROW": "1"}])
 def test_dispatch_knobs_do_not_change_results(engine, env, monkeypatch):
     """Wave split, kernel-variant choice and chunk geometry are scheduling only:
