@@ -58,6 +58,7 @@ class BatchRun:
     results: list[InstanceResult]
     seconds_lower: float
     seconds_device: float
+    raw: object = None  # engine.RawResults of the run
 
 
 def run_specs(specs: list[InstanceSpec], engine: Engine | None = None,
@@ -69,7 +70,7 @@ def run_specs(specs: list[InstanceSpec], engine: Engine | None = None,
     raw = eng.run(low, log=log)
     t2 = time.perf_counter()
     modes = [sp.deployment.mode for sp in specs]
-    return BatchRun(low, split_results(low, raw, modes), t1 - t0, t2 - t1)
+    return BatchRun(low, split_results(low, raw, modes), t1 - t0, t2 - t1, raw)
 
 
 def device_request_arrays(configs: list[DeploymentConfig], engine: Engine | None = None):
@@ -126,6 +127,69 @@ def _metrics_or_failure(res: InstanceResult) -> MetricsBundle | Failure:
         return compute_metrics(res)
     except Exception as exc:  # IncompleteTrace (e.g. no requests), metrics.py:115-121
         return Failure(exc)
+
+
+def metrics_many(run: BatchRun) -> list[MetricsBundle | Failure]:
+    """[_metrics_or_failure(r) for r in run.results] with the metric rows and replica
+    rows read once as Python values (numpy scalar access per field is the cost of
+    compute_metrics at sweep scale); identical bundles (tests/test_batch_host.py)."""
+    from .metrics import IncompleteTrace
+    res = run.results
+    raw = run.raw
+    if raw is None or not res:
+        return [_metrics_or_failure(r) for r in res]
+    rows, rep = raw.rows, raw.replica_out
+    col = {f: rows[f].tolist() for f in ("status", "total_tokens", "makespan_s",
+                                        "throughput_tokens_per_s_per_gpu", "bubble_fraction",
+                                        "avg_input_tokens", "avg_output_tokens", "af_steps",
+                                        "ttft", "tpot", "e2e", "af_busy_fraction")}
+    rbusy, rsteps = rep["busy_fraction"].tolist(), rep["steps_executed"].tolist()
+    roff = run.lowered.descs["replica_offset"].tolist()
+    nan = math.isnan
+
+    def agg(v):
+        return None if nan(v[1]) else {"mean": v[0], "p50": v[1], "p90": v[2], "p99": v[3]}
+
+    out = []
+    for i, r in enumerate(res):
+        if col["status"][i] != 0:
+            out.append(Failure(r.error()))
+            continue
+        if len(r.request_ids) == 0:
+            out.append(Failure(IncompleteTrace("trace contains no requests")))
+            continue
+        pv = r.per_request_values
+        per_request = {rid: {"ttft_s": a, "tpot_s": b, "e2e_s": c}
+                       for rid, a, b, c in zip(r.request_ids, *pv)}
+        busy = {}
+        o = roff[i]
+        for j, k in enumerate(r.replica_keys):
+            if rsteps[o + j] > 0:
+                busy[k] = rbusy[o + j]
+        if col["af_steps"][i] > 0:
+            for j, name in enumerate(abi.AF_RESOURCES):
+                busy[name] = col["af_busy_fraction"][i][j]
+        busy = dict(sorted(busy.items()))
+        if r.expert_imbalance is not None:
+            imbalance = r.expert_imbalance
+        elif r.batches is not None:
+            imbalance = [round(x, 6) for b in r.batches if b["moe_ratio"] is not None
+                         for x in b["moe_ratio"]]
+        else:
+            imbalance = None if r.has_moe else []
+        thr = col["throughput_tokens_per_s_per_gpu"][i]
+        bub = col["bubble_fraction"][i]
+        out.append(MetricsBundle(
+            per_request=per_request, ttft=agg(col["ttft"][i]), tpot=agg(col["tpot"][i]),
+            e2e=agg(col["e2e"][i]), total_tokens=col["total_tokens"][i],
+            makespan_s=col["makespan_s"][i], total_gpus=r.total_gpus,
+            throughput_tokens_per_s_per_gpu=thr, busy_fraction=busy,
+            bubble_fraction=None if nan(bub) else bub, expert_imbalance=imbalance,
+            workload_summary={"batch_size": len(r.request_ids),
+                              "avg_input_tokens": col["avg_input_tokens"][i],
+                              "avg_output_tokens": col["avg_output_tokens"][i],
+                              "throughput_tokens_per_s_per_gpu": thr}))
+    return out
 
 
 def attach_expert_imbalance(specs: list[InstanceSpec], results: list[InstanceResult],
@@ -285,8 +349,8 @@ def _simulate_local(configs, engine, base_dir, device_workload, expert_imbalance
         run = run_specs(specs, engine)
         if expert_imbalance:
             attach_expert_imbalance(specs, run.results, engine)
-        for i, res in zip(where, run.results):
-            out[i] = _metrics_or_failure(res)
+        for i, m in zip(where, metrics_many(run)):
+            out[i] = m
     return out
 
 

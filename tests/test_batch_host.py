@@ -104,3 +104,28 @@ def test_shared_request_ids_are_ranked_like_python_strings():
         rank = np.empty(n, np.int64)
         rank[order] = np.arange(n)
         assert (_id_ranks(ids) == rank).all()
+
+
+def test_metrics_many_equals_compute_metrics(golden_scenarios):
+    """api.metrics_many (row fields read once per batch) builds exactly the bundles
+    (or failures) compute_metrics builds instance by instance."""
+    from oracle.oracle import OracleEngine
+    from paper_2508_03148_b200.api import _metrics_or_failure, metrics_many, run_specs
+    docs = [copy.deepcopy(g["config"]) for g in golden_scenarios.values()]
+    docs += W.c5_sweep(n_seeds=1, n_requests=8, configs=list(range(0, 64, 9)))
+    specs = []
+    for d in docs:
+        try:
+            specs.append(instance_spec(parse_config(d)))
+        except Exception:
+            continue
+    run = run_specs(specs, OracleEngine(threads=4))
+    want = [_metrics_or_failure(r) for r in run.results]
+    got = metrics_many(run)
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        if isinstance(b, Failure):
+            assert isinstance(a, Failure) and a.status == b.status
+        else:
+            assert a.to_dict() == b.to_dict()
+    assert any(isinstance(b, Failure) for b in want) and not all(isinstance(b, Failure) for b in want)
