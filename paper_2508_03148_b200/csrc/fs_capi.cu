@@ -223,7 +223,8 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
     int c;
     if (lrn) c = fs::kSimLearned;
     else if (d.has_moe && d.num_experts >= 64 && !no_longrow) c = fs::kSimLongRow;
-    else if (d.has_moe && d.mode == FS_MODE_COLOCATED && e->comoe_variant) c = fs::kSimCoMoe;
+    else if (d.has_moe && d.mode == FS_MODE_COLOCATED && d.top_k <= 3 && e->comoe_variant)
+      c = fs::kSimCoMoe;
     else if (d.has_moe || !e->dense_variant) c = fs::kSimAnalytic;
     else c = fs::kSimDense;
     cls[i] = c;

@@ -2021,6 +2021,8 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
   if (FS_DENSE_ONLY && d->has_moe) fail(I, FS_ERR_INTERNAL, 9);  // host dispatch error
   if ((I.mode == FS_MODE_PD && !FS_HAS_PD) || (I.mode == FS_MODE_AF && !FS_HAS_AF))
     fail(I, FS_ERR_INTERNAL, 10);  // host dispatch error: mode not compiled into this variant
+  if (FS_KCAP_MAX <= 4 && d->has_moe && d->top_k + 1 > 4 && d->top_k < d->num_experts)
+    fail(I, FS_ERR_INTERNAL, 11);  // host dispatch error: top_k beyond this variant's lists
 #if FS_LEARNED
   {
     const int fsel[2] = {d->attn_forest, d->gg_forest};
