@@ -433,6 +433,194 @@ __global__ void __launch_bounds__(kC2Threads) attention_cost_kernel_tma(
   }
 }
 
+// ---- four threads per batch, asynchronous copies ("g4a", the default) ------------------------
+// A group of four threads reduces four consecutive batches one after another,
+// the four threads taking interleaved 16-byte pieces of each batch (thread j
+// the int4s j, j+4, ...), so every 64 contiguous bytes are read by one load
+// instruction's four lanes and only ~57 K batches are partly consumed at any
+// time (the thread-per-batch kernel: ~227 K, about the L2, and ~30% of its
+// bytes re-read from DRAM). Per member: sums of l, c, l*c and of l*c where
+// c == l, and min/max trackers instead of per-member flag logic; the
+// validation flags are formed once per batch from them (the same predicates as
+// acc4). Thread j then runs batch j's fp64 tail, so the tail uses every lane.
+struct G4Acc {
+  int64_t sq, skv, sall, seq;
+  int minl, maxl, mincl, maxcl;  // min / max of l and of c - l
+};
+__device__ __forceinline__ void g4_init(G4Acc& a) {
+  a.sq = a.skv = a.sall = a.seq = 0;
+  a.minl = a.mincl = 0x7fffffff;
+  a.maxl = a.maxcl = (int)0x80000000;
+}
+// products and the c == l split; min/max of l and c - l (validity: l >= 1 and
+// c >= l, plus l == 1 for decode -- then c >= 1 follows)
+__device__ __forceinline__ void g4_track(G4Acc& a, int l, int c) {
+  const int64_t lc = (int64_t)l * c;
+  a.sall += lc;
+  if (c == l) a.seq += lc;
+  const int d = c - l;  // wraps only for c < 0 (then min(d, c) < 0 flags it anyway)
+  a.minl = min(a.minl, l);
+  a.maxl = max(a.maxl, l);
+  a.mincl = min(a.mincl, min(d, c));
+  a.maxcl = max(a.maxcl, d);
+}
+__device__ __forceinline__ void g4_member(G4Acc& a, int l, int c) {
+  a.sq += l;
+  a.skv += c;
+  g4_track(a, l, c);
+}
+// four members: the sums of l and of c in two 32-bit pair sums (exact for
+// valid members, each in [1, 2^31); an invalid batch's sums are never used)
+__device__ __forceinline__ void g4_piece(G4Acc& a, const int4& x, const int4& y) {
+  a.sq += (int64_t)(uint64_t)((uint32_t)x.x + (uint32_t)x.y) +
+          (int64_t)(uint64_t)((uint32_t)x.z + (uint32_t)x.w);
+  a.skv += (int64_t)(uint64_t)((uint32_t)y.x + (uint32_t)y.y) +
+           (int64_t)(uint64_t)((uint32_t)y.z + (uint32_t)y.w);
+  g4_track(a, x.x, y.x); g4_track(a, x.y, y.y);
+  g4_track(a, x.z, y.z); g4_track(a, x.w, y.w);
+}
+__device__ __forceinline__ void g4_reduce(G4Acc& a) {
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    a.sq += __shfl_xor_sync(FS_FULL, a.sq, o);
+    a.skv += __shfl_xor_sync(FS_FULL, a.skv, o);
+    a.sall += __shfl_xor_sync(FS_FULL, a.sall, o);
+    a.seq += __shfl_xor_sync(FS_FULL, a.seq, o);
+    a.minl = min(a.minl, __shfl_xor_sync(FS_FULL, a.minl, o));
+    a.maxl = max(a.maxl, __shfl_xor_sync(FS_FULL, a.maxl, o));
+    a.mincl = min(a.mincl, __shfl_xor_sync(FS_FULL, a.mincl, o));
+    a.maxcl = max(a.maxcl, __shfl_xor_sync(FS_FULL, a.maxcl, o));
+  }
+}
+// the batch's flags and the exactness guard's bound: every l*c <= max l * max c
+// and max c <= max(c - l) + max l
+__device__ __forceinline__ bool g4_bad(const G4Acc& a, bool d, bool empty) {
+  return !empty && (a.minl < 1 || a.mincl < 0 || (d && a.maxl != 1));
+}
+__device__ __forceinline__ int64_t g4_bound(const G4Acc& a) {
+  return (int64_t)max(a.maxl, 0) * max((int64_t)a.maxcl + a.maxl, (int64_t)0);
+}
+
+// Each thread's 16-byte pieces of the NEXT batch are copied global -> shared
+// memory with cp.async (LDGSTS) while the current batch is reduced from shared
+// memory: the bytes in flight cost no registers, so an SM keeps about a batch
+// per thread in the air. A thread reads back only what it copied itself
+// (cp.async.wait_group), so no barrier is needed. Slots hold kG4aSlots pieces
+// per array per thread (an 80-member batch); longer batches read the rest from
+// global memory. Needs 16-byte aligned length arrays (else: tpb).
+#ifndef FS_C2_G4A_THREADS
+#define FS_C2_G4A_THREADS 128
+#endif
+#ifndef FS_C2_G4A_SLOTS
+#define FS_C2_G4A_SLOTS 5
+#endif
+constexpr int kG4aThreads = FS_C2_G4A_THREADS;
+constexpr int kG4aSlots = FS_C2_G4A_SLOTS;
+
+__device__ __forceinline__ void g4a_copy16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kG4aThreads) attention_cost_kernel_g4a(
+    const int32_t* __restrict__ q, const int32_t* __restrict__ kv,
+    const int64_t* __restrict__ off, const uint8_t* __restrict__ dec, int64_t nb,
+    fs_attn_params prm, double* __restrict__ out, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) int4 g4a_smem[];  // [stage][array][slot][thread]
+  fs_cost_ctx h;
+  h.peak_flops = prm.peak_flops; h.mem_bw = prm.mem_bw; h.kernel_overhead_us = prm.kernel_overhead_us;
+  h.tp = h.ep = h.moe_tp = h.pp = 1;
+  const int tid = threadIdx.x, j = tid & 3;
+  const int64_t grp = ((int64_t)blockIdx.x * kG4aThreads + tid) >> 2;
+  const int64_t ngrp = ((int64_t)gridDim.x * kG4aThreads) >> 2;
+  auto slot = [&](int st, int arr, int i) -> int4* {
+    return g4a_smem + (((st * 2 + arr) * kG4aSlots + i) * kG4aThreads + tid);
+  };
+  // the n-th batch this group handles: groups of four consecutive batches, grid-strided
+  auto bidx = [&](int64_t n) { return (grp + (n >> 2) * ngrp) * 4 + (n & 3); };
+  auto body = [&](int64_t o0, int64_t o1, int64_t& a0, int64_t& n4) {
+    a0 = min(o1, (o0 + 3) & ~(int64_t)3);
+    n4 = (o1 - a0) >> 2;
+  };
+  auto issue = [&](int st, int64_t o0, int64_t o1) {
+    int64_t a0, n4;
+    body(o0, o1, a0, n4);
+#pragma unroll
+    for (int i = 0; i < kG4aSlots; i++) {
+      const int64_t pi = j + 4 * i;
+      if (pi < n4) {
+        g4a_copy16(slot(st, 0, i), q + a0 + 4 * pi);
+        g4a_copy16(slot(st, 1, i), kv + a0 + 4 * pi);
+      }
+    }
+  };
+  struct Off { int64_t o0, o1; bool d, valid; };
+  auto load_off = [&](int64_t n, Off& r) {
+    const int64_t b = bidx(n);
+    r.valid = b < nb;
+    r.o0 = r.valid ? __ldg(off + b) : 0;
+    r.o1 = r.valid ? __ldg(off + b + 1) : 0;
+    r.d = r.valid && __ldg(dec + b) != 0;
+  };
+  Off A, B, C;
+  load_off(0, A);
+  load_off(1, B);
+  if (A.valid) issue(0, A.o0, A.o1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int64_t m_sq = 0, m_skv = 0, m_seq = 0, m_sall = 0, m_o0 = 0, m_o1 = 0;
+  int64_t m_mlc = 0;
+  int m_bad = 0;
+  bool m_d = false;
+  for (int64_t n = 0;; n++) {
+    const int64_t b = bidx(n);
+    if ((b & ~(int64_t)3) >= nb) break;  // this group's four batches are past the end
+    const int k = (int)(n & 3);
+    if (B.valid) issue((int)((n + 1) & 1), B.o0, B.o1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    load_off(n + 2, C);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    if (A.valid) {
+      const int st = (int)(n & 1);
+      const int64_t o0 = A.o0, o1 = A.o1;
+      const bool d = A.d;
+      G4Acc a;
+      g4_init(a);
+      int64_t a0, n4;
+      body(o0, o1, a0, n4);
+      if (o0 + j < a0) g4_member(a, __ldg(q + o0 + j), __ldg(kv + o0 + j));
+      const int4* sb = g4a_smem + st * 2 * kG4aSlots * kG4aThreads + tid;
+#pragma unroll
+      for (int i = 0; i < kG4aSlots; i++) {
+        if (j + 4 * i < n4) g4_piece(a, sb[i * kG4aThreads], sb[(kG4aSlots + i) * kG4aThreads]);
+      }
+      const int4* q4 = reinterpret_cast<const int4*>(q + a0);
+      const int4* k4 = reinterpret_cast<const int4*>(kv + a0);
+#pragma unroll 1
+      for (int64_t i = j + 4 * kG4aSlots; i < n4; i += 4) {  // beyond the slots
+        const int4 x = __ldg(q4 + i), y = __ldg(k4 + i);
+        g4_piece(a, x, y);
+      }
+      const int64_t t = a0 + 4 * n4 + j;
+      if (t < o1) g4_member(a, __ldg(q + t), __ldg(kv + t));
+      g4_reduce(a);
+      if (j == k) {
+        m_bad = g4_bad(a, d, o1 <= o0);
+        m_sq = a.sq; m_skv = a.skv; m_seq = a.seq; m_sall = a.sall;
+        m_mlc = g4_bound(a); m_o0 = o0; m_o1 = o1; m_d = d;
+      }
+    }
+    if (k == 3) {
+      const int64_t bj = (b & ~(int64_t)3) + j;
+      if (bj < nb)
+        c2_finish(bj, m_d, m_sq, m_skv, m_seq, m_sall - m_seq, m_mlc, m_bad, m_o0,
+                  m_o1, q, kv, prm, h, out, status);
+    }
+    A = B;
+    B = C;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // ---- synthetic workload generation (workload.py:131-216) --------------------------------------
 // One thread per (instance, stream): numpy's streams are sequential (variable
 // word consumption: ziggurat slow paths, Lemire rejections), so each stream is
@@ -600,8 +788,8 @@ int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* of
                           int32_t* status, int n_sms, void* stream) {
   if (nb <= 0) return 0;
   const int threads = 256;
-  // "tpb" (default: 166 us for 2^20 x 72-request batches), "tma" (181 us: DRAM reads
-  // exactly the algorithmic bytes, latency bound on the member loop), "warp"
+  // "g4a" (default: 127 us for 2^20 x 72-request batches, DRAM reads = the algorithmic
+  // bytes), "tpb" (167 us, +30% DRAM re-reads), "tma" (181 us), "warp"
   const char* mode = getenv("FS_C2");
   if (mode != nullptr && strcmp(mode, "tma") == 0) {
     static bool configured = false;
@@ -618,6 +806,26 @@ int launch_attention_cost(const int32_t* q, const int32_t* kv, const int64_t* of
     int64_t blocks = (int64_t)n_sms * per;
     if (blocks > tiles) blocks = tiles;
     attention_cost_kernel_tma<<<(int)blocks, kC2Threads, sizeof(C2Smem), (cudaStream_t)stream>>>(
+        q, kv, off, dec, nb, prm, out, status);
+    return 1;
+  }
+  const bool al16 = ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kv)) & 15) == 0;
+  if ((mode == nullptr || strcmp(mode, "g4a") == 0) && al16) {
+    const int bytes = 2 * 2 * kG4aSlots * kG4aThreads * 16;
+    static bool g4a_configured = false;
+    if (!g4a_configured) {
+      cudaFuncSetAttribute(attention_cost_kernel_g4a, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           bytes);
+      g4a_configured = true;
+    }
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, attention_cost_kernel_g4a, kG4aThreads,
+                                                  bytes);
+    if (per < 1) per = 1;
+    int64_t blocks = (nb + kG4aThreads - 1) / kG4aThreads;
+    const int64_t cap = (int64_t)n_sms * per;
+    if (blocks > cap) blocks = cap;
+    attention_cost_kernel_g4a<<<(int)blocks, kG4aThreads, bytes, (cudaStream_t)stream>>>(
         q, kv, off, dec, nb, prm, out, status);
     return 1;
   }

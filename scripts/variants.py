@@ -1,7 +1,8 @@
 """Compile-time variants of the analytic simulation kernel, built here and timed on the GPU.
 
   python scripts/variants.py build NAME "-DFLAG=1 ..." [NAME "FLAGS" ...]
-      compiles fs_engine.cu with the flags into paper_2508_03148_b200/lib/variants/NAME.so
+      compiles fs_engine.cu (or the SRC=file.cu named among the flags) with the flags
+      into paper_2508_03148_b200/lib/variants/NAME.so
       (linked with the standard objects of the other translation units)
   python scripts/variants.py timeenv SEEDS "FS_X=1,FS_Y=2" ...
       GPU: the default library under runtime knobs (environment), one process each
@@ -28,13 +29,16 @@ def build(pairs):
     procs = []
     for name, flags in pairs:
         obj = os.path.join(VDIR, name + ".o")
-        cmd = [native.nvcc(), *native.NVCC_FLAGS, *flags.split(), "-c", "-o", obj,
-               os.path.join(native.CSRC, "fs_engine.cu")]
-        procs.append((name, obj, subprocess.Popen(cmd)))
-    for name, obj, p in procs:
+        # a token SRC=file.cu picks the translation unit to vary (default fs_engine.cu)
+        src = next((f[4:] for f in flags.split() if f.startswith("SRC=")), "fs_engine.cu")
+        fl = [f for f in flags.split() if not f.startswith("SRC=")]
+        cmd = [native.nvcc(), *native.NVCC_FLAGS, *fl, "-c", "-o", obj,
+               os.path.join(native.CSRC, src)]
+        procs.append((name, obj, src, subprocess.Popen(cmd)))
+    for name, obj, src, p in procs:
         if p.wait() != 0:
             raise SystemExit(f"variant {name} failed to compile")
-        others = [native._obj(s) for s in native.SOURCES if s != "fs_engine.cu"]
+        others = [native._obj(s) for s in native.SOURCES if s != src]
         subprocess.run([native.nvcc(), *native.ARCH, "-shared", "-o",
                         os.path.join(VDIR, name + ".so"), obj, *others], check=True)
         print("built", name)

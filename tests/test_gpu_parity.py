@@ -117,7 +117,7 @@ def test_attention_cost_bulk_vs_oracle(engine):
         assert out[b] == oracle.attention_us(bool(dec[b]), q[s:e], kv[s:e], 32, 8, 128, 2.25e15, 8e12)
 
 
-@pytest.mark.parametrize("mode", ["tpb", "tma", "warp"])
+@pytest.mark.parametrize("mode", ["tpb", "tma", "warp", "g4a"])
 def test_attention_cost_kernel_variants_agree(engine, mode, monkeypatch):
     """Every C2 kernel variant (FS_C2) gives the default's bits, incl. ragged,
     empty and invalid batches and an unaligned CSR start."""
@@ -129,11 +129,18 @@ def test_attention_cost_kernel_variants_agree(engine, mode, monkeypatch):
     n = int(off[-1])
     kv = np.clip(rs.lognormal(6.5, 1.4, size=n), 1, 32768).astype(np.int32)
     dec = (np.arange(3000) % 2).astype(np.uint8)
-    q = kv.copy()
+    q = np.maximum(1, kv - rs.integers(0, 3, size=n)).astype(np.int32)  # c == l and c > l
     for b in range(3000):
         if dec[b]:
             q[off[b]:off[b + 1]] = 1
-    q[off[500]] = 0                                   # invalid member
+    q[off[500]] = 0                                   # invalid members: l < 1,
+    kv[off[900]] = np.iinfo(np.int32).min             # c < 0 (c - l wraps in int32),
+    q[off[701]] = 2                                   # a decode member with l != 1,
+    kv[off[703]] = 0                                  # a decode member with c < 1,
+    kv[off[902]] = q[off[902]] - 1                    # a prefill member with c < l
+    for b in (500, 900, 701, 703, 902):
+        assert off[b + 1] > off[b] and bool(dec[b]) == (b % 2 == 1)
+    q[off[1000]:off[1001]] = kv[off[1000]:off[1001]] = 2 ** 30  # past the exact-integer guard
     p = attn_params(32, 8, 128, 2, 2.25e15, 8e12, 5.0)
     monkeypatch.delenv("FS_C2", raising=False)
     want, wst = engine.attention_cost(q, kv, off, dec, p)
@@ -141,6 +148,8 @@ def test_attention_cost_kernel_variants_agree(engine, mode, monkeypatch):
     got, gst = engine.attention_cost(q, kv, off, dec, p)
     assert (gst == wst).all()
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    assert all(wst[b] != 0 for b in (500, 900, 701, 703, 902)) and wst[1000] == 0
+    assert (wst == 0).sum() > 2500
 
 
 def test_sweep_driver_end_to_end(engine, tmp_path):
