@@ -52,13 +52,22 @@ def instance_spec(config: DeploymentConfig, requests=None) -> InstanceSpec:
     return spec
 
 
-@dataclass
 class BatchRun:
-    lowered: Lowered
-    results: list[InstanceResult]
-    seconds_lower: float
-    seconds_device: float
-    raw: object = None  # engine.RawResults of the run
+    """A device run of lowered instances: `results` (one InstanceResult per
+    instance) is built on first access -- metrics_many reads the lowered and raw
+    columns directly and never needs it."""
+
+    def __init__(self, lowered: Lowered, raw, modes: list[str], seconds_lower: float,
+                 seconds_device: float):
+        self.lowered, self.raw, self.modes = lowered, raw, modes
+        self.seconds_lower, self.seconds_device = seconds_lower, seconds_device
+        self._results: list[InstanceResult] | None = None
+
+    @property
+    def results(self) -> list[InstanceResult]:
+        if self._results is None:
+            self._results = split_results(self.lowered, self.raw, self.modes)
+        return self._results
 
 
 def run_specs(specs: list[InstanceSpec], engine: Engine | None = None,
@@ -70,7 +79,7 @@ def run_specs(specs: list[InstanceSpec], engine: Engine | None = None,
     raw = eng.run(low, log=log)
     t2 = time.perf_counter()
     modes = [sp.deployment.mode for sp in specs]
-    return BatchRun(low, split_results(low, raw, modes), t1 - t0, t2 - t1, raw)
+    return BatchRun(low, raw, modes, t1 - t0, t2 - t1)
 
 
 def device_request_arrays(configs: list[DeploymentConfig], engine: Engine | None = None):
@@ -129,63 +138,94 @@ def _metrics_or_failure(res: InstanceResult) -> MetricsBundle | Failure:
         return Failure(exc)
 
 
+_HOSTPY: list = []
+
+
+def _hostpy():
+    """csrc/fs_hostpy.c (per-request dictionaries in C), or None if not built."""
+    if not _HOSTPY:
+        from .native import load_hostpy
+        _HOSTPY.append(load_hostpy())
+    return _HOSTPY[0]
+
+
 def metrics_many(run: BatchRun) -> list[MetricsBundle | Failure]:
-    """[_metrics_or_failure(r) for r in run.results] with the metric rows and replica
-    rows read once as Python values (numpy scalar access per field is the cost of
-    compute_metrics at sweep scale); identical bundles (tests/test_batch_host.py)."""
-    from .metrics import IncompleteTrace
-    res = run.results
-    raw = run.raw
-    if raw is None or not res:
-        return [_metrics_or_failure(r) for r in res]
+    """[_metrics_or_failure(r) for r in run.results], built from the lowered and raw
+    columns read once as Python values (numpy scalar access per field, and one
+    InstanceResult per instance, are the cost of compute_metrics at sweep scale);
+    identical bundles (tests/test_batch_host.py). InstanceResults are used only for
+    failed instances and when a run carries logs or attached expert imbalance."""
+    from .metrics import IncompleteTrace, _per_request_columns
+    raw, low = run.raw, run.lowered
+    if raw is None:
+        return [_metrics_or_failure(r) for r in run.results]
+    n_inst = low.n_instances
+    if n_inst == 0:
+        return []
+    have = run._results  # InstanceResults, when something already built them
+    if have is None and raw.log is not None:
+        have = run.results  # batch logs: expert imbalance per instance
     rows, rep = raw.rows, raw.replica_out
     col = {f: rows[f].tolist() for f in ("status", "total_tokens", "makespan_s",
                                         "throughput_tokens_per_s_per_gpu", "bubble_fraction",
                                         "avg_input_tokens", "avg_output_tokens", "af_steps",
                                         "ttft", "tpot", "e2e", "af_busy_fraction")}
     rbusy, rsteps = rep["busy_fraction"].tolist(), rep["steps_executed"].tolist()
-    roff = run.lowered.descs["replica_offset"].tolist()
+    descs = low.descs
+    roff = descs["replica_offset"].tolist()
+    qoff, qn = descs["req_offset"].tolist(), descs["n_requests"].tolist()
+    gpus, moe = descs["total_gpus"].tolist(), descs["has_moe"].tolist()
+    ttft_c, tpot_c, e2e_c = (_per_request_columns(low, raw) if low.n_requests
+                             else ([], [], []))
     nan = math.isnan
+    host = _hostpy()
 
     def agg(v):
         return None if nan(v[1]) else {"mean": v[0], "p50": v[1], "p90": v[2], "p99": v[3]}
 
     out = []
-    for i, r in enumerate(res):
+    for i in range(n_inst):
         if col["status"][i] != 0:
+            r = have[i] if have is not None else split_results(low, raw, run.modes, only=i)
             out.append(Failure(r.error()))
             continue
-        if len(r.request_ids) == 0:
+        ids = low.request_ids[i]
+        if len(ids) == 0:
             out.append(Failure(IncompleteTrace("trace contains no requests")))
             continue
-        pv = r.per_request_values
-        per_request = {rid: {"ttft_s": a, "tpot_s": b, "e2e_s": c}
-                       for rid, a, b, c in zip(r.request_ids, *pv)}
+        o, n = qoff[i], qn[i]
+        if host is not None and type(ids) is list:
+            per_request = host.per_request(ids, ttft_c, tpot_c, e2e_c, o)
+        else:
+            per_request = {rid: {"ttft_s": a, "tpot_s": b, "e2e_s": c}
+                           for rid, a, b, c in zip(ids, ttft_c[o:o + n], tpot_c[o:o + n],
+                                                   e2e_c[o:o + n])}
         busy = {}
-        o = roff[i]
-        for j, k in enumerate(r.replica_keys):
-            if rsteps[o + j] > 0:
-                busy[k] = rbusy[o + j]
+        ro = roff[i]
+        for j, k in enumerate(low.replica_keys[i]):
+            if rsteps[ro + j] > 0:
+                busy[k] = rbusy[ro + j]
         if col["af_steps"][i] > 0:
             for j, name in enumerate(abi.AF_RESOURCES):
                 busy[name] = col["af_busy_fraction"][i][j]
         busy = dict(sorted(busy.items()))
-        if r.expert_imbalance is not None:
+        r = have[i] if have is not None else None
+        if r is not None and r.expert_imbalance is not None:
             imbalance = r.expert_imbalance
-        elif r.batches is not None:
+        elif r is not None and r.batches is not None:
             imbalance = [round(x, 6) for b in r.batches if b["moe_ratio"] is not None
                          for x in b["moe_ratio"]]
         else:
-            imbalance = None if r.has_moe else []
+            imbalance = None if moe[i] else []
         thr = col["throughput_tokens_per_s_per_gpu"][i]
         bub = col["bubble_fraction"][i]
         out.append(MetricsBundle(
             per_request=per_request, ttft=agg(col["ttft"][i]), tpot=agg(col["tpot"][i]),
             e2e=agg(col["e2e"][i]), total_tokens=col["total_tokens"][i],
-            makespan_s=col["makespan_s"][i], total_gpus=r.total_gpus,
+            makespan_s=col["makespan_s"][i], total_gpus=gpus[i],
             throughput_tokens_per_s_per_gpu=thr, busy_fraction=busy,
             bubble_fraction=None if nan(bub) else bub, expert_imbalance=imbalance,
-            workload_summary={"batch_size": len(r.request_ids),
+            workload_summary={"batch_size": len(ids),
                               "avg_input_tokens": col["avg_input_tokens"][i],
                               "avg_output_tokens": col["avg_output_tokens"][i],
                               "throughput_tokens_per_s_per_gpu": thr}))

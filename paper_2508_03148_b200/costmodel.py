@@ -136,6 +136,8 @@ def check_model_slots(attention_model: LearnedModel | None,
 def check_model_slots_engine(attention_model: LearnedModel | None,
                              grouped_gemm_model: LearnedModel | None) -> None:
     """check_model_slots plus the engine's forest size limit."""
+    if attention_model is None and grouped_gemm_model is None:
+        return
     from .abi import MAX_FOREST_TREES
     from .errors import EngineCapacityError
     check_model_slots(attention_model, grouped_gemm_model)

@@ -368,12 +368,12 @@ def lower(specs: list[InstanceSpec]) -> Lowered:
     descs["n_requests"] = n_req
     descs["req_offset"] = req_off
     descs["replica_offset"] = rep_off
-    trace: list[int] = []
     n_pref = np.fromiter((len(t.prefix_suffix) for t in tmpl_of), dtype=np.int64, count=n)
     pref_off = np.concatenate([[0], np.cumsum(n_pref)[:-1]]) if n else n_pref
-    for i, t in enumerate(tmpl_of):
-        descs[i]["trace_offset"] = len(trace)
-        trace.extend(t.trace)
+    n_tr = np.fromiter((len(t.trace) for t in tmpl_of), dtype=np.int64, count=n)
+    if n:
+        descs["trace_offset"] = np.concatenate([[0], np.cumsum(n_tr)[:-1]])
+    trace: list[int] = [c for t in tmpl_of for c in t.trace]
     # replicas: template rows with prefix indices made global
     if n:
         # gather template rows: row j of instance i = template row (tbase[which[i]] + j)

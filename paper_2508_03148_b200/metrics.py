@@ -123,15 +123,17 @@ class InstanceResult:
         return [self.request_ids[i] for i in order if self.completion_rank[i] >= 0]
 
 
-def _per_request_columns(low, raw) -> tuple[list, list, list]:
-    """ttft / tpot / e2e of every request of the batch as Python floats, in one
-    vectorised pass with the reference's expressions (metrics.py:91-100): exact
-    int64 ns differences, then the same IEEE divisions Python performs."""
-    arr = low.arrival
+def _per_request_columns(low, raw, o: int = 0, n: int | None = None) -> tuple[list, list, list]:
+    """ttft / tpot / e2e of every request of the batch (or of requests [o, o+n)) as
+    Python floats, in one vectorised pass with the reference's expressions
+    (metrics.py:91-100): exact int64 ns differences, then the same IEEE divisions
+    Python performs."""
+    e = len(low.arrival) if n is None else o + n
+    arr = low.arrival[o:e]
     with np.errstate(all="ignore"):
-        ttft = (raw.first_ns - arr) / 1e9
-        e2e = (raw.done_ns - arr) / 1e9
-        n_out = low.output.astype(np.int64)
+        ttft = (raw.first_ns[o:e] - arr) / 1e9
+        e2e = (raw.done_ns[o:e] - arr) / 1e9
+        n_out = low.output[o:e].astype(np.int64)
         tpot = (e2e - ttft) / (n_out - 1)
     tp = tpot.tolist()
     for j in np.flatnonzero(n_out <= 1).tolist():
@@ -139,24 +141,35 @@ def _per_request_columns(low, raw) -> tuple[list, list, list]:
     return ttft.tolist(), tp, e2e.tolist()
 
 
-def split_results(low, raw, modes: list[str]) -> list[InstanceResult]:
+def split_results(low, raw, modes: list[str], only: int | None = None):
+    """One InstanceResult per instance (views into the batch arrays); `only`: just
+    that instance's, returned alone."""
     out = []
-    cols = _per_request_columns(low, raw) if low.n_requests else ([], [], [])
-    for i in range(low.n_instances):
-        d = low.descs[i]
-        o, n = int(d["req_offset"]), int(d["n_requests"])
-        ro, nr = int(d["replica_offset"]), int(d["n_replicas"])
+    if only is None:
+        cols = _per_request_columns(low, raw) if low.n_requests else ([], [], [])
+    descs = low.descs
+    f = {k: descs[k].tolist() for k in ("req_offset", "n_requests", "replica_offset",
+                                        "n_replicas", "total_gpus", "has_moe",
+                                        "kv_bytes_per_token", "af_micro_batches")}
+    pool = low.replicas["kv_pool_tokens"].tolist()
+    for i in (range(low.n_instances) if only is None else (only,)):
+        o, n = f["req_offset"][i], f["n_requests"][i]
+        ro, nr = f["replica_offset"][i], f["n_replicas"][i]
+        if only is None:
+            pv = (cols[0][o:o + n], cols[1][o:o + n], cols[2][o:o + n])
+        else:
+            pv = _per_request_columns(low, raw, o, n)
         res = InstanceResult(
             index=i, row=raw.rows[i], replica_keys=low.replica_keys[i],
             replica_out=raw.replica_out[ro:ro + nr], request_ids=low.request_ids[i],
             arrival_ns=low.arrival[o:o + n], prompt=low.prompt[o:o + n],
             output=low.output[o:o + n], first_token_ns=raw.first_ns[o:o + n],
             done_ns=raw.done_ns[o:o + n], completion_rank=raw.done_rank[o:o + n],
-            total_gpus=int(d["total_gpus"]), mode=modes[i],
-            pool_capacity=low.replicas["kv_pool_tokens"][ro:ro + nr].tolist(),
-            has_moe=bool(d["has_moe"]), kv_bytes_per_token=int(d["kv_bytes_per_token"]),
-            af_micro_batches=int(d["af_micro_batches"]),
-            per_request_values=(cols[0][o:o + n], cols[1][o:o + n], cols[2][o:o + n]))
+            total_gpus=f["total_gpus"][i], mode=modes[i],
+            pool_capacity=pool[ro:ro + nr],
+            has_moe=bool(f["has_moe"][i]), kv_bytes_per_token=f["kv_bytes_per_token"][i],
+            af_micro_batches=f["af_micro_batches"][i],
+            per_request_values=pv)
         if raw.log is not None:
             if raw.log.spec.batch_cap:
                 res.batches = raw.log.instance_batches(i)
@@ -166,7 +179,7 @@ def split_results(low, raw, modes: list[str]) -> list[InstanceResult]:
             if raw.log.spec.event_cap and res.ok and not res.log_truncated:
                 res.event_log = raw.log.instance_events(i)
         out.append(res)
-    return out
+    return out[0] if only is not None else out
 
 
 def _nan_to_none(x: float) -> float | None:

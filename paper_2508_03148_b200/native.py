@@ -70,8 +70,44 @@ def _compile(src: str, verbose: bool, extra: list[str]) -> str:
     return out
 
 
+HOSTPY_SRC = os.path.join(CSRC, "fs_hostpy.c")
+
+
+def hostpy_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "lib", "_fs_host" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_hostpy(force: bool = False) -> str:
+    """The CPython host helper (csrc/fs_hostpy.c; gcc, in-tree next to the engine)."""
+    import sysconfig
+    target = hostpy_path()
+    if not force and not _stale(target, [HOSTPY_SRC]):
+        return target
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+                    "-o", target + ".tmp", HOSTPY_SRC], check=True)
+    os.replace(target + ".tmp", target)
+    return target
+
+
+def load_hostpy():
+    """The _fs_host module, or None when it is not built (pure-Python fallback:
+    the same dictionaries, slower)."""
+    import importlib.util
+    path = hostpy_path()
+    if not os.path.exists(path):
+        return None
+    spec = importlib.util.spec_from_file_location("_fs_host", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
           out: str | None = None) -> str:
+    if out is None and not extra:
+        build_hostpy(force)
     target = out or LIB
     if not force and not extra and not stale() and os.path.exists(target):
         return target

@@ -120,8 +120,14 @@ def test_metrics_many_equals_compute_metrics(golden_scenarios):
         except Exception:
             continue
     run = run_specs(specs, OracleEngine(threads=4))
+    got = metrics_many(run)  # from the batch columns: no InstanceResult built
+    assert run._results is None
     want = [_metrics_or_failure(r) for r in run.results]
-    got = metrics_many(run)
+    again = metrics_many(run)  # and through the InstanceResults
+
+    def key(b):
+        return b.status if isinstance(b, Failure) else b.to_dict()
+    assert [key(b) for b in again] == [key(b) for b in got]
     assert len(got) == len(want)
     for a, b in zip(got, want):
         if isinstance(b, Failure):
