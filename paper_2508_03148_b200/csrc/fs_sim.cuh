@@ -78,13 +78,36 @@ constexpr int kLayerChunk = 32;
 constexpr int kSlabBytes = 12 * 1024;  // per-warp shared-memory slab for hot instance state
 constexpr int32_t kNoFinish = 0x7fffffff;
 
+#ifndef FS_TERM_MEMO  // memo of the batch terms that depend on n alone (analytic variants):
+#define FS_TERM_MEMO (!FS_LEARNED)  // C5 dense wave 40.9 -> 30 ms, MoE wave -5 ms
+#endif
+constexpr int kMemoSlots = 32;  // direct-mapped on n_tokens (a decode batch's n <= 32 maps 1:1)
+// One memo line: the n-only terms of execute_batch (qkv, out, ffn, tp all-reduce,
+// pp transfers) for one (n, cost context); the context is compared bit for bit.
+struct TermMemo {
+  double qkv, out, ffn, coll, pp;
+  double peak, bw, ovh;
+  int64_t n;
+  int32_t tp, ppd;
+};
+
 struct __align__(16) WarpSmem {
   uint64_t keys[kLayerChunk][2];
   int64_t af_attn[FS_MAX_MICRO_BATCHES];
   int64_t af_xfer[FS_MAX_MICRO_BATCHES];
   int32_t af_size[FS_MAX_MICRO_BATCHES];
   int32_t af_stage[FS_MAX_MICRO_BATCHES];
+#if FS_TERM_MEMO && FS_DENSE_ONLY
+  union {  // the dense variant never routes, so the tally space holds the memo
+    int counts[FS_MAX_EXPERTS];
+    TermMemo memo[kMemoSlots];
+  };
+#else
   int counts[FS_MAX_EXPERTS];
+#if FS_TERM_MEMO
+  TermMemo memo[kMemoSlots];
+#endif
+#endif
 #if FS_LEARNED
   double fx[17];                   // learned attention model: feature vector
   double fvals[kMaxForestTrees];   // ... and per-tree leaf values
@@ -123,8 +146,15 @@ __device__ __forceinline__ void fail(Inst& I, int st, int detail) {
 }
 
 // ---- replica state: every lane loads the same struct; lane 0 stores -------------
+// Every write of a replica state is store_rep (lane 0, then __syncwarp) or the
+// initialisation loop (followed by __syncwarp), so a load needs no barrier of
+// its own; store_rep's leading barrier orders the other lanes' loads before the
+// overwrite.
+#ifndef FS_LOADREP_SYNC
+#define FS_LOADREP_SYNC 0
+#endif
 __device__ __forceinline__ RepState load_rep(const EngineParams& P, const Inst& I, int r) {
-  __syncwarp();
+  if (FS_LOADREP_SYNC) __syncwarp();
   return I.rs[r];
 }
 __device__ __forceinline__ void store_rep(const EngineParams& P, const Inst& I, int r,
@@ -1028,6 +1058,45 @@ __device__ __forceinline__ BatchTerms batch_terms(const fs_instance_desc* d, con
   return t;
 }
 
+// attention_us_from(attn_flops, sum_q, sum_kv) alone (batch_terms' lane 1 term)
+__device__ __forceinline__ double attention_term(const fs_instance_desc* d, const fs_cost_ctx& c,
+                                                 const BatchShape& b) {
+  int hq, hkv;
+  heads_of(d, c.tp, hq, hkv);
+  return attention_us_from(b.attn_flops, b.sum_q, b.sum_kv, hq, hkv, d->head_dim, c,
+                           d->dtype_bytes);
+}
+
+#if FS_TERM_MEMO
+// batch_terms with the n-only terms memoised per instance (the attention term
+// depends on the batch's context sums and is always evaluated); bit-identical
+// values, since a hit returns exactly what batch_terms computed for that n and
+// context.
+__device__ __forceinline__ BatchTerms batch_terms_memo(const fs_instance_desc* d,
+                                                       const fs_cost_ctx& c, const BatchShape& b,
+                                                       int lane, WarpSmem* sm) {
+  TermMemo& m = sm->memo[b.n_tokens & (kMemoSlots - 1)];
+  if (m.n == b.n_tokens && m.tp == c.tp && m.ppd == c.pp &&
+      __double_as_longlong(m.peak) == __double_as_longlong(c.peak_flops) &&
+      __double_as_longlong(m.bw) == __double_as_longlong(c.mem_bw) &&
+      __double_as_longlong(m.ovh) == __double_as_longlong(c.kernel_overhead_us)) {
+    BatchTerms t;
+    t.qkv = m.qkv; t.out = m.out; t.ffn = m.ffn; t.coll = m.coll; t.pp = m.pp;
+    t.att = attention_term(d, c, b);
+    return t;
+  }
+  const BatchTerms t = batch_terms(d, c, b, lane);
+  __syncwarp();
+  if (lane == 0) {
+    m.qkv = t.qkv; m.out = t.out; m.ffn = t.ffn; m.coll = t.coll; m.pp = t.pp;
+    m.peak = c.peak_flops; m.bw = c.mem_bw; m.ovh = c.kernel_overhead_us;
+    m.n = b.n_tokens; m.tp = c.tp; m.ppd = c.pp;
+  }
+  __syncwarp();
+  return t;
+}
+#endif
+
 // Duration in us (same on all lanes). moe_out (global) receives the per-layer
 // moe_imbalance values round(expert / mean(per_rank), 6) when non-null.
 __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_replica_desc& rd,
@@ -1037,7 +1106,11 @@ __device__ double execute_batch(const EngineParams& P, Inst& I, int r, const fs_
   const fs_cost_ctx c = rd.cost;
   const int L = d->num_layers;
   const int64_t n = b.n_tokens;
+#if FS_TERM_MEMO
+  const BatchTerms bt = batch_terms_memo(d, c, b, I.lane, sm);
+#else
   const BatchTerms bt = batch_terms(d, c, b, I.lane);
+#endif
   const double qkv = bt.qkv, out = bt.out, coll = bt.coll;
 #if FS_LEARNED
   const double att = isnan(b.learned_attn) ? bt.att : b.learned_attn;
@@ -2037,6 +2110,10 @@ __device__ void simulate_instance(const EngineParams& P, int idx, int lane, int 
 #else
   // the host picks the learned variant for any instance with a model
   if (d->attn_forest != -1 || d->gg_forest != -1) fail(I, FS_ERR_INTERNAL, 8);
+#endif
+#if FS_TERM_MEMO
+  // the memo holds the previous instance's model: invalidate
+  for (int i = lane; i < kMemoSlots; i += 32) sm->memo[i].n = -1;
 #endif
   for (int r = lane; r < I.R; r += 32) {
     RepState s;

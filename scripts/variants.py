@@ -49,7 +49,12 @@ def time_one(seeds: int):
 
     from bench import lower_docs, workload_docs
     from paper_2508_03148_b200.engine import Engine
-    low = lower_docs(workload_docs(0, seeds, 64))
+    docs = workload_docs(0, seeds, 64)
+    fams = os.environ.get("FS_FAMILIES")  # e.g. "AB": the dense families of C5 only
+    if fams:
+        fam_of = ["A"] * 16 + ["B"] * 32 + ["C"] * 16
+        docs = [d for i, d in enumerate(docs) if fam_of[i // seeds] in fams]
+    low = lower_docs(docs)
     eng = Engine(0)
     eng.stage(low)
     eng.launch()
