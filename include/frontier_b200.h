@@ -382,7 +382,8 @@ int fs_stage(fs_engine* e,
  * Fails (and launches nothing) when the staged batch uses learned models and
  * fs_set_forests replaced them after fs_stage. */
 int fs_launch_async(fs_engine* e, void* stream);
-/* Copy results of the last launch to host buffers (synchronizes the stream). */
+/* Copy results of the last launch to host buffers: waits for that launch only (on
+ * whichever stream it ran), so another engine's batch keeps running meanwhile. */
 int fs_fetch(fs_engine* e, fs_metric_row* rows_out, fs_replica_out* replica_out,
              fs_request_out per_request);
 /* Kernel launches issued by the last fs_launch_async. */

@@ -195,3 +195,19 @@ class OracleEngine:
 
     def run(self, low: Lowered, log: LogSpec | None = None, log_sizes: dict | None = None):
         return run(low, log=log, threads=self.threads, log_sizes=log_sizes)
+
+    # the Engine's stage / launch / fetch / peer, as api.simulate's pipeline uses them
+    def stage(self, low: Lowered) -> None:
+        self._staged, self._result = low, None
+
+    def launch(self, stream_ptr=None) -> None:
+        self._result = run(self._staged, threads=self.threads)
+
+    def fetch(self, low: Lowered | None = None, per_request: bool = True):
+        return self._result
+
+    def peer(self) -> "OracleEngine":
+        p = getattr(self, "_peer", None)
+        if p is None:
+            p = self._peer = OracleEngine(self.threads)
+        return p

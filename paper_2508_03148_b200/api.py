@@ -361,9 +361,25 @@ def simulate(configs: list, engine: Engine | None = None, base_dir: str = ".",
         return _simulate_local(configs, engine, base_dir, device_workload, expert_imbalance)
 
 
+PIPELINE_MIN = 256  # instances below which simulate() runs one batch
+
+
+def _pipeline_groups(parsed: list, pre: list) -> list[list[int]]:
+    """simulate()'s batches, in launch order: the MoE configs first (the longest device
+    wave), then the rest, so building and lowering the second batch on the host runs
+    while the first is on the GPU, and metrics of the first are built while the second
+    runs. Small or single-family inputs stay one batch. Instances are independent, so
+    the split changes no result (tests/test_gpu_parity.py)."""
+    ok = [i for i, c in enumerate(parsed) if c is not None and not isinstance(pre[i], Exception)]
+    if len(ok) < PIPELINE_MIN:
+        return [ok]
+    moe = [i for i in ok if parsed[i].model.moe is not None]
+    rest = [i for i in ok if parsed[i].model.moe is None]
+    return [g for g in (moe, rest) if g]
+
+
 def _simulate_local(configs, engine, base_dir, device_workload, expert_imbalance):
     out: list[MetricsBundle | Failure | None] = [None] * len(configs)
-    specs, where = [], []
     parsed: list = [None] * len(configs)
     for i, p in enumerate(parse_all(configs, base_dir)):
         if isinstance(p, Failure):
@@ -375,20 +391,34 @@ def _simulate_local(configs, engine, base_dir, device_workload, expert_imbalance
         ok = [i for i in range(len(configs)) if parsed[i] is not None]
         for i, r in zip(ok, device_request_arrays([parsed[i] for i in ok], engine)):
             pre[i] = r
-    for i, cfg in enumerate(parsed):
-        if cfg is None:
+    for i, r in enumerate(pre):
+        if isinstance(r, Exception):
+            out[i] = Failure(r)
+    eng = engine or default_engine()
+    launched = []  # (engine, lowered, specs, where), each batch on its own engine
+    for g, idx in enumerate(_pipeline_groups(parsed, pre)):
+        specs, where = [], []
+        for i in idx:
+            try:
+                specs.append(instance_spec(parsed[i], requests=pre[i]))
+                where.append(i)
+            except Exception as exc:  # config-time failures (cli.py:229-233)
+                out[i] = Failure(exc)
+        if not specs:
             continue
-        try:
-            if isinstance(pre[i], Exception):
-                raise pre[i]
-            specs.append(instance_spec(cfg, requests=pre[i]))
-            where.append(i)
-        except Exception as exc:  # config-time failures (cli.py:229-233)
-            out[i] = Failure(exc)
-    if specs:
-        run = run_specs(specs, engine)
+        e = eng if g == 0 else eng.peer()
+        t0 = time.perf_counter()
+        low = lower(specs)
+        e.stage(low)
+        e.launch()
+        launched.append((e, low, specs, where, time.perf_counter() - t0))
+    for e, low, specs, where, t_low in launched:
+        t1 = time.perf_counter()
+        raw = e.fetch(low)
+        run = BatchRun(low, raw, [sp.deployment.mode for sp in specs], t_low,
+                       time.perf_counter() - t1)
         if expert_imbalance:
-            attach_expert_imbalance(specs, run.results, engine)
+            attach_expert_imbalance(specs, run.results, e)
         for i, m in zip(where, metrics_many(run)):
             out[i] = m
     return out

@@ -42,6 +42,8 @@ struct fs_engine {
   int n_sms = 148;
   std::string err;
   cudaStream_t stream = nullptr;
+  cudaEvent_t launched = nullptr;  // recorded after a batch's last kernel (fs_fetch waits on it)
+  cudaEvent_t staged_ev = nullptr; // recorded after fs_stage's uploads + midstate kernel
   // inputs
   DevBuf descs, reps, prefixes, mid, trace, arrival, prompt, output, id_rank, order;
   // workspace
@@ -138,7 +140,13 @@ int fs_create(int device, fs_engine** out) {
   e->dense_variant = env_int("FS_DENSE_VARIANT", 1);
   e->comoe_variant = env_int("FS_COMOE_VARIANT", 1);
   e->chunk_blocks = env_int("FS_CHUNK_BLOCKS", 96);
-  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->launched, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&e->staged_ev, cudaEventDisableTiming) != cudaSuccess) {
+    if (e->launched) cudaEventDestroy(e->launched);
+    if (e->launched) cudaEventDestroy(e->launched);
+  if (e->staged_ev) cudaEventDestroy(e->staged_ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
     return 5;
   }
@@ -271,6 +279,12 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   FS_CHECK(upload(e->list_base, list_base.data(), list_base.size(), s));
   FS_CHECK(upload(e->heap_base, heap_base.data(), heap_base.size(), s));
   FS_CHECK(upload(e->af_base, af_base.data(), af_base.size(), s));
+  // The caller's arrays may be pinned (truly asynchronous copies): wait for the
+  // uploads, but not for the memsets and the midstate kernel below -- another engine's
+  // resident wave can hold every SM they could run on (api.simulate stages its second
+  // batch then); fs_launch_async orders itself after staged_ev instead.
+  FS_CHECK(cudaEventRecord(e->staged_ev, s));
+  FS_CHECK(cudaEventSynchronize(e->staged_ev));
   const size_t nr = (size_t)std::max<int64_t>(n_requests, 1);
   FS_CHECK(e->first.ensure(nr * 8));
   FS_CHECK(e->done.ensure(nr * 8));
@@ -387,7 +401,7 @@ int fs_stage(fs_engine* e, const fs_instance_desc* descs, int32_t n_instances,
   e->n_req = n_requests;
   fs::launch_midstate(P.prefixes, e->mid.as<uint32_t>(), n_prefixes, s);
   FS_CHECK(cudaGetLastError());
-  FS_CHECK(cudaStreamSynchronize(s));
+  FS_CHECK(cudaEventRecord(e->staged_ev, s));
   e->staged = 1;
   return 0;
 }
@@ -401,6 +415,7 @@ int fs_launch_async(fs_engine* e, void* stream) {
     return 14;
   }
   cudaStream_t s = stream ? (cudaStream_t)stream : e->stream;
+  FS_CHECK(cudaStreamWaitEvent(s, e->staged_ev, 0));
   FS_CHECK(cudaMemsetAsync(e->work.p, 0, sizeof(int32_t), s));
   FS_CHECK(cudaMemsetAsync(e->inst_done.p, 0, 2 * sizeof(int32_t), s));
   if (e->params.jobs)
@@ -430,6 +445,7 @@ int fs_launch_async(fs_engine* e, void* stream) {
   }
   e->last_launches += fs::launch_metrics(e->params, s);
   FS_CHECK(cudaGetLastError());
+  FS_CHECK(cudaEventRecord(e->launched, s));
   return 0;
 }
 
@@ -437,7 +453,9 @@ int fs_fetch(fs_engine* e, fs_metric_row* rows_out, fs_replica_out* replica_out,
              fs_request_out pr) {
   if (!e || !e->staged) return 1;
   cudaStream_t s = e->stream;
-  FS_CHECK(cudaDeviceSynchronize());
+  // wait for this engine's batch only (the launch may have been on the caller's
+  // stream): another engine's batch on the same device keeps running meanwhile
+  FS_CHECK(cudaStreamWaitEvent(s, e->launched, 0));
   if (rows_out)
     FS_CHECK(cudaMemcpyAsync(rows_out, e->rows.p, sizeof(fs_metric_row) * e->n_inst,
                              cudaMemcpyDeviceToHost, s));

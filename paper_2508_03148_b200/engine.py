@@ -326,6 +326,15 @@ class Engine:
         self._check(rc, "fs_stage")
         self._staged = low
 
+    def peer(self) -> "Engine":
+        """A second engine on the same device (own staging buffers and stream), kept
+        for the life of this one: lets a caller stage and launch the next batch while
+        this engine's batch is still on the device (api.simulate's pipeline)."""
+        p = getattr(self, "_peer", None)
+        if p is None:
+            p = self._peer = Engine(self.device)
+        return p
+
     def launch(self, stream_ptr: int | None = None) -> None:
         self._check(self.lib.fs_launch_async(self.h, stream_ptr), "fs_launch_async")
 

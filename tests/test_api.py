@@ -74,3 +74,27 @@ def test_sweep_override_failure_is_a_row(eng, tmp_path):
     assert [r[2].split(":")[0] for r in rows[1:]] == ["ok", "ok", "failed"]
     assert summary["ok"] == 2
     assert json.load(open(tmp_path / "frontier.json"))
+
+
+def test_pipelined_batches_equal_one_batch(eng, golden_scenarios, monkeypatch):
+    """simulate() splits a large mixed input into a MoE batch and a dense batch on two
+    engines (api._pipeline_groups); every bundle and failure equals the one-batch run."""
+    import paper_2508_03148_b200.api as api
+    names = ["co_moe_mixtral_ep2", "co_llama_40", "pd_moe_mixtral", "af_dense_m4",
+             "af_tiny_moe_m3_dp2"]
+    docs = [golden_scenarios[n]["config"] for n in names]
+    bad = copy.deepcopy(docs[1])
+    bad["clusters"][0]["num_replicas"] = 0
+    docs.insert(2, bad)
+    one = simulate(copy.deepcopy(docs), engine=eng)
+    monkeypatch.setattr(api, "PIPELINE_MIN", 2)
+    groups = api._pipeline_groups(
+        [api.parse_config(copy.deepcopy(d)) if i != 2 else None for i, d in enumerate(docs)],
+        [None] * len(docs))
+    assert groups == [[0, 3, 5], [1, 4]]
+    two = simulate(copy.deepcopy(docs), engine=eng)
+    for a, b in zip(one, two):
+        if isinstance(a, Failure):
+            assert isinstance(b, Failure) and a.status == b.status
+        else:
+            assert a.to_dict() == b.to_dict()

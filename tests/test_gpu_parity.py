@@ -246,3 +246,20 @@ def test_per_variant_waves_match_solo_runs(engine):
         assert solo.rows.tobytes() == batch.rows[i:i + 1].tobytes(), i
         assert np.array_equal(solo.first_ns, batch.first_ns[o:o + n]), i
         assert np.array_equal(solo.done_ns, batch.done_ns[o:o + n]), i
+
+
+def test_simulate_pipeline_on_two_engines(engine, monkeypatch):
+    """simulate() on a mixed C5 slice: the MoE batch on the engine and the dense batch on
+    its peer, launched back to back (the second staged while the first runs), give the
+    same bundles as one batch, and the same as the C oracle."""
+    import paper_2508_03148_b200.api as api
+    from oracle.oracle import OracleEngine
+    from paper_2508_03148_b200.api import simulate
+    docs = W.c5_sweep(n_seeds=2, n_requests=24, configs=list(range(0, 64, 3)))
+    one = simulate(copy.deepcopy(docs), engine=engine, device_workload=True)
+    monkeypatch.setattr(api, "PIPELINE_MIN", 2)
+    two = simulate(copy.deepcopy(docs), engine=engine, device_workload=True)
+    ref = simulate(copy.deepcopy(docs), engine=OracleEngine(threads=8))
+    assert any(d["model"].get("moe") for d in docs) and any(not d["model"].get("moe") for d in docs)
+    for a, b, c in zip(one, two, ref):
+        assert a.to_dict() == b.to_dict() == c.to_dict()
