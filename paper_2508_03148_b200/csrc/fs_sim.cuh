@@ -379,6 +379,9 @@ constexpr int kMaxChunks = 1 << 18;
 #define FS_CHUNK_BLOCKS 96
 #endif
 constexpr int kChunkBlocks = FS_CHUNK_BLOCKS;
+#ifndef FS_ROWS_PATH  // whole-row, whole-block routing passes for top_k == 2 (process_rows)
+#define FS_ROWS_PATH 1
+#endif
 #ifndef FS_NSEG_ROWS  // rows are split into lane segments while rows * nseg stays below this
 #define FS_NSEG_ROWS 64  // 64: C5 224-226 ms; 256: 225-228; 2048 (round 1): ~228; 4096: 232-236
 #endif
@@ -608,6 +611,109 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
   if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, FS_ERR_ROUTING_TIE);
 }
 
+// Whole rows per lane (nseg == 1) of whole Philox blocks (E % 4 == 0, so a row's draws
+// start block-aligned): the row's E/4 blocks with no per-draw range predicates, 32-bit
+// expert indices and a sorted list of exactly k+1 surrogate keys (k+1 min/max pairs
+// per draw). Same selection, tie test and exact redo as process_chunk_k; this is
+// every decode-batch call of the C5 Mixtral family.
+template <int KC>
+__device__ void process_rows(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
+                             int lane, int* tally) {
+  constexpr int k = KC - 1;
+  const int64_t T = __ldcg(&job->T);
+  const int E = __ldcg(&job->E), nl = __ldcg(&job->nl);
+  const int ppc = __ldcg(&job->passes_per_chunk);
+  const int64_t total_rows = (int64_t)nl * T;
+  int eb = 0;
+  while ((1 << eb) < E) eb++;
+  const uint32_t keep = ~((1u << eb) - 1u);
+  const int nblk = E >> 2;
+  int tie = 0;
+  const int64_t row0 = (int64_t)c * ppc * 32;
+  const int64_t row_end = min(total_rows, row0 + (int64_t)ppc * 32);
+  int64_t row_j = row0 + lane;
+  int layer = (int)(row_j / T);
+  int64_t r = row_j - (int64_t)layer * T;
+  int key_layer = -1;
+  uint64_t k0 = 0, k1 = 0;
+  const int l_first = (int)(row0 / T);
+  const int span = row_end > row0 ? (int)((row_end - 1) / T) - l_first + 1 : 0;
+  const bool local = span * E <= FS_MAX_EXPERTS;
+  if (local) {
+    for (int i = lane; i < span * E; i += 32) tally[i] = 0;
+    __syncwarp();
+  }
+  for (int64_t pass0 = row0; pass0 < row_end; pass0 += 32) {
+    const bool active = row_j < row_end;
+    uint32_t top[KC];
+#pragma unroll
+    for (int j = 0; j < KC; j++) top[j] = 0xFFFFFFFFu;
+    if (active) {
+      if (layer != key_layer) {
+        k0 = __ldcg(&job->keys[layer][0]);
+        k1 = __ldcg(&job->keys[layer][1]);
+        key_layer = layer;
+      }
+      const uint64_t b0 = (uint64_t)r * (uint64_t)nblk + 1;  // numpy pre-increments
+#pragma unroll 1
+      for (int q = 0; q < nblk; q++) {
+        const U4 blk = philox4x64_10(b0 + q, k0, k1);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uint32_t x = ((uint32_t)(blk.v[j] >> 32) & keep) | (uint32_t)(4 * q + j);
+#pragma unroll
+          for (int t = 0; t < KC; t++) {
+            const uint32_t lo = min(top[t], x);
+            x = max(top[t], x);
+            top[t] = lo;
+          }
+        }
+      }
+    }
+    const bool unsure = active && (top[k] >> eb) == (top[k - 1] >> eb);
+    int ids[k];
+#pragma unroll
+    for (int j = 0; j < k; j++) ids[j] = (int)(top[j] & ~keep);
+    if (__any_sync(FS_FULL, unsure)) {
+      // exact 64-bit redo of this pass (as process_chunk_k)
+      uint64_t t64[KC];
+#pragma unroll
+      for (int j = 0; j < KC; j++) t64[j] = ~0ull;
+      uint64_t thr = ~0ull;
+      const uint64_t rb = (uint64_t)r * (uint64_t)E;
+      if (active) topk_scan<KC>(t64, KC, thr, rb, rb + E, rb, k0, k1);
+#pragma unroll
+      for (int j = 0; j < k; j++) ids[j] = (int)(t64[j] & 0x7FF);
+      if (active && (t64[k] >> 11) == (t64[k - 1] >> 11)) tie = 1;
+    }
+    if (local) {
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < k; j++) atomicAdd(&tally[(layer - l_first) * E + ids[j]], 1);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < k; j++) {
+        const int key = active ? layer * E + ids[j] : -1;
+        const unsigned grp = __match_any_sync(FS_FULL, key);
+        if (key >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counts[key], __popc(grp));
+      }
+    }
+    r += 32;
+    row_j += 32;
+    while (r >= T) { r -= T; layer++; }
+  }
+  if (local) {
+    __syncwarp();
+    for (int i = lane; i < span * E; i += 32) {
+      const int v = tally[i];
+      if (v) atomicAdd(&counts[l_first * E + i], v);
+    }
+    __syncwarp();
+  }
+  if (__any_sync(FS_FULL, tie) && lane == 0) atomicExch(&job->tie, FS_ERR_ROUTING_TIE);
+}
+
 #if FS_LEARNED
 // dirichlet_skew: chunk c is the whole router call of layer c (its exponentials are
 // one stream with data-dependent word consumption); the claimant draws it with its
@@ -639,6 +745,11 @@ __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* cou
     if (publish && lane == 0) red_add_release_i32(&job->done, 1);
     return;
   }
+#endif
+#if FS_ROWS_PATH
+  if (__ldcg(&job->nseg) == 1 && (__ldcg(&job->E) & 3) == 0 && k == 2)
+    process_rows<3>(P, job, counts, c, lane, tally);
+  else
 #endif
   if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane, tally);
 #if FS_KCAP_MAX > 4
