@@ -379,7 +379,7 @@ constexpr int kMaxChunks = 1 << 18;
 #define FS_CHUNK_BLOCKS 96
 #endif
 constexpr int kChunkBlocks = FS_CHUNK_BLOCKS;
-#ifndef FS_ROWS_PATH  // whole-row, whole-block routing passes for top_k == 2 (process_rows)
+#ifndef FS_ROWS_PATH  // whole-row, whole-block routing passes for top_k 1-3 and 8 (process_rows)
 #define FS_ROWS_PATH 1
 #endif
 #ifndef FS_NSEG_ROWS  // rows are split into lane segments while rows * nseg stays below this
@@ -615,7 +615,7 @@ __device__ void process_chunk_k(const EngineParams& P, RouteJob* job, int32_t* c
 // start block-aligned): the row's E/4 blocks with no per-draw range predicates, 32-bit
 // expert indices and a sorted list of exactly k+1 surrogate keys (k+1 min/max pairs
 // per draw). Same selection, tie test and exact redo as process_chunk_k; this is
-// every decode-batch call of the C5 Mixtral family.
+// every decode-batch call of the C5 Mixtral family (k = 2) and of DeepSeek-V3 (k = 8).
 template <int KC>
 __device__ void process_rows(const EngineParams& P, RouteJob* job, int32_t* counts, int c,
                              int lane, int* tally) {
@@ -657,7 +657,11 @@ __device__ void process_rows(const EngineParams& P, RouteJob* job, int32_t* coun
       const uint64_t b0 = (uint64_t)r * (uint64_t)nblk + 1;  // numpy pre-increments
 #pragma unroll 1
       for (int q = 0; q < nblk; q++) {
+#if FS_LONG_ROW_UNROLL
+        const U4 blk = philox4x64_10_unrolled(b0 + q, k0, k1);  // long rows: see pass_fast
+#else
         const U4 blk = philox4x64_10(b0 + q, k0, k1);
+#endif
 #pragma unroll
         for (int j = 0; j < 4; j++) {
           uint32_t x = ((uint32_t)(blk.v[j] >> 32) & keep) | (uint32_t)(4 * q + j);
@@ -747,8 +751,13 @@ __device__ void process_chunk(const EngineParams& P, RouteJob* job, int32_t* cou
   }
 #endif
 #if FS_ROWS_PATH
-  if (__ldcg(&job->nseg) == 1 && (__ldcg(&job->E) & 3) == 0 && k == 2)
-    process_rows<3>(P, job, counts, c, lane, tally);
+  const bool rows = __ldcg(&job->nseg) == 1 && (__ldcg(&job->E) & 3) == 0;
+  if (rows && k == 2) process_rows<3>(P, job, counts, c, lane, tally);
+  else if (rows && k == 1) process_rows<2>(P, job, counts, c, lane, tally);
+  else if (rows && k == 3) process_rows<4>(P, job, counts, c, lane, tally);
+#if FS_KCAP_MAX > 4
+  else if (rows && k == 8) process_rows<9>(P, job, counts, c, lane, tally);  // DeepSeek-V3
+#endif
   else
 #endif
   if (k + 1 <= 4) process_chunk_k<4>(P, job, counts, c, lane, tally);
