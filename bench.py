@@ -102,6 +102,18 @@ def routing_peak():
             "unrolled_best": max(unrolled) * 1e9, "source": "profiles/philox_peak_r2.json"}
 
 
+def imad_wide_rate():
+    """Measured IMAD.WIDE.U32 lane-ops per clock per SM (scripts/micro/imad_rates.cu)."""
+    try:
+        for line in open(os.path.join(ROOT, "profiles", "imad_rates_r2.json")):
+            r = json.loads(line)
+            if r.get("op") == "imad_wide32":
+                return float(r["ops_per_clk_per_sm"])
+    except Exception:
+        pass
+    return None
+
+
 def cpu_count() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -374,7 +386,7 @@ def bench_configs(device: int, reps: int = 2):
     return out
 
 
-def routing_line(draws: int, step_ms: float) -> dict:
+def routing_line(draws: int, step_ms: float, sm_mhz: float | None = None) -> dict:
     rate = draws / (step_ms / 1e3)
     pk = routing_peak()
     out = {"draws_per_step": draws, "draws_per_s": rate,
@@ -385,6 +397,16 @@ def routing_line(draws: int, step_ms: float) -> dict:
         out.update({"peak": pk["rolled_8_warps_per_sm"], "frac": rate / pk["rolled_8_warps_per_sm"],
                     "peak_best_occupancy": pk["rolled_best"], "peak_unrolled": pk["unrolled_best"],
                     "peak_source": pk["source"]})
+    # the multiplier bound: 80 IMAD.WIDE.U32 per Philox4x64-10 block at
+    # the measured 25.6 lane-ops per clock per SM (profiles/imad_rates_r2.json)
+    wide = imad_wide_rate()
+    if wide:
+        blocks_peak = wide * 148 * (sm_mhz or 1965.0) * 1e6 / 80
+        out["imad_wide_bound"] = {"unit": "Philox blocks/s", "achieved": rate / 4,
+                                  "peak": blocks_peak, "frac": rate / 4 / blocks_peak,
+                                  "imad_wide_per_block": 80,
+                                  "lane_ops_per_clk_per_sm": wide,
+                                  "source": "profiles/imad_rates_r2.json"}
     return out
 
 
@@ -656,7 +678,8 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_kind},
             "issue": issue,
             "api_end_to_end": api,
-            "routing": routing_line(draws_per_step * world, max_ms / args.steps),
+            "routing": routing_line(draws_per_step * world, max_ms / args.steps,
+                                    (clocks.summary() or {}).get("sm_max_mhz")),
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": launches_per_step * args.steps,
