@@ -263,3 +263,42 @@ def test_simulate_pipeline_on_two_engines(engine, monkeypatch):
     assert any(d["model"].get("moe") for d in docs) and any(not d["model"].get("moe") for d in docs)
     for a, b, c in zip(one, two, ref):
         assert a.to_dict() == b.to_dict() == c.to_dict()
+
+
+@pytest.mark.parametrize("experts,top_k", [(8, 1), (8, 3), (12, 2), (16, 3), (32, 8), (10, 2),
+                                           (64, 1), (64, 3), (128, 8)])
+def test_routing_shapes_vs_oracle(engine, experts, top_k):
+    """Router shapes around the whole-row pass (process_rows: nseg == 1, E % 4 == 0,
+    top_k 1-3 and 8) and outside it (E % 4 != 0), on the sweep, analytic and long-row
+    kernels: device == oracle on every output (statuses included), and every router
+    call of a completed instance tallies exactly T * top_k expert slots."""
+    from oracle import oracle
+    from parity import run_backend
+    base = [d for d in W.c5_sweep(n_seeds=1, n_requests=24) if d["model"].get("moe")]
+    docs = []
+    for j, d in enumerate(base[::3]):
+        d = copy.deepcopy(d)
+        d["model"]["moe"]["num_experts"] = experts
+        d["model"]["moe"]["top_k"] = top_k
+        cl = d["clusters"][0]
+        ep0 = ep = cl.get("parallelism", {}).get("ep", 1)
+        while experts % ep:
+            ep //= 2
+        cl.setdefault("parallelism", {})["ep"] = ep
+        cl["gpus_per_replica"] = cl["gpus_per_replica"] // ep0 * ep  # = tp * pp * ep
+        d["seed"] = 31 + j
+        docs.append(d)
+    low = lower([instance_spec(parse_config(copy.deepcopy(d))) for d in docs])
+    dev = engine.run(low)
+    # large expert counts at ep 1-2 leave no KV room (RequestCannotFit, as the reference)
+    assert (dev.rows["status"] == 0).sum() >= 2, dev.rows["status"]
+    ref = oracle.run(low, threads=8)
+    assert (dev.rows["status"] == ref.rows["status"]).all()
+    ok = dev.rows["status"] == 0  # a failed instance's row carries no metrics
+    assert (dev.first_ns == ref.first_ns).all() and (dev.done_ns == ref.done_ns).all()
+    for f in ROW_FIELDS:
+        a, b = dev.rows[f][ok], ref.rows[f][ok]
+        assert np.all((a == b) | (np.isnan(a) & np.isnan(b)) if a.dtype.kind == "f" else a == b), f
+    for r in run_backend(engine, docs, routes=True):
+        for rt in (r.routes or []) if r.ok else []:
+            assert sum(rt["counts"]) == rt["tokens"] * top_k
